@@ -1,0 +1,210 @@
+/*
+ * lbm.h -- C-ABI of the B200-native (sm_100a) D3Q19 lattice Boltzmann library
+ * implementing the hot path of Fu & Song, "Designing a 3D Parallel
+ * Memory-Aware Lattice Boltzmann Algorithm on Manycore Systems"
+ * (arXiv 2208.05429): the fused collide + stream update with bounce-back
+ * walls and a moving lid ("Fuse Swap LBM", Alg. 1), with
+ * two collision-streaming cycles merged per sweep (Alg. 2),
+ * X-slab partitioned across GPUs.
+ *
+ * Plain C types only: no torch or CUDA types cross this boundary (streams
+ * and device pointers are passed as void* / double*).  Every function
+ * returns an lbm_status and never aborts; lbm_last_error() gives the reason.
+ *
+ * Conventions shared by all calls
+ * -------------------------------
+ *  Domain      nx * ny * nz cells, all fluid.  The
+ *              moving lid is the top z face z = nz-1 (R-5), with
+ *              tangential velocity u_lid (u_lid[2] must be 0).
+ *  Directions  canonical D3Q19 order i = 0..18 of SPEC.md:109 (directions
+ *              1..9 lexicographically negative, opp(i) = i +- 9).
+ *  Host arrays C order, z fastest.  rho[x][y][z]; u[x][y][z][3] (component
+ *              fastest); populations f[i][x][y][z].  Always double, whatever
+ *              the lattice dtype (fp32 lattices convert on copy).  With an
+ *              X-slab partition (world > 1) every host/device array covers
+ *              the caller's slab only: nx_local = nx / world planes starting
+ *              at global x0 = rank * nx_local.
+ *  Time        lbm_init_equilibrium / lbm_set_populations set the canonical
+ *              state f(t0); lbm_step(n) advances it to f(t0 + n), where one
+ *              step is collide then stream; the read-back
+ *              calls return the canonical f(t) and its moments.
+ *  Ownership   the context owns every device buffer, stream, event and
+ *              communicator it creates; the caller owns all arrays it
+ *              passes.  Host-array calls copy synchronously before
+ *              returning; the caller may reuse the array immediately.
+ *  Errors      LBM_EINVAL for invalid arguments (checked before any
+ *              allocation or launch); LBM_ENOMEM for a failed allocation;
+ *              LBM_ECUDA / LBM_ENCCL for a CUDA or NCCL failure, after which
+ *              the context is poisoned and every later call except
+ *              lbm_last_error / lbm_destroy returns LBM_ESTATE.  Errors of
+ *              asynchronous work surface at the next blocking call.
+ *  Threads     a context is not thread-safe; distinct contexts are
+ *              independent.
+ */
+#ifndef LBM_B200_H
+#define LBM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LBM_ABI_VERSION 1
+
+typedef struct lbm_ctx lbm_ctx; /* opaque; library-owned */
+
+typedef enum { LBM_F64 = 0, LBM_F32 = 1 } lbm_dtype;
+
+/* Boundary mode.  CAVITY: link-wise (half-way) bounce-back on all six faces
+ * and the moving lid on z = nz-1 (R-4..R-7; SPEC.md:164-182;
+ * BASELINE.json configs 1, 2, 4, 5).  PERIODIC: wrap on all three axes
+ * (BASELINE.json config 3), u_lid ignored. */
+typedef enum { LBM_BC_CAVITY = 0, LBM_BC_PERIODIC = 1 } lbm_bc;
+
+typedef enum {
+    LBM_OK = 0,
+    LBM_EINVAL = 1,
+    LBM_ENOMEM = 2,
+    LBM_ECUDA = 3,
+    LBM_ENCCL = 4,
+    LBM_ESTATE = 5
+} lbm_status;
+
+/* Sweep kernel selection.  K1: one fused collide+stream step per HBM pass
+ * (Alg. 1's loop fusion).  K2: two steps per HBM pass, temporally blocked
+ * in shared memory (Alg. 2's two-step merge); an odd remainder uses K1.
+ * AUTO picks K2 where available.  Results are bitwise identical. */
+typedef enum { LBM_KERNEL_AUTO = 0, LBM_KERNEL_K1 = 1, LBM_KERNEL_K2 = 2 } lbm_kernel;
+
+/* Halo transport between X-slabs (PAPER.md:336 X-only partition).
+ *  NONE   world == 1 and local_slabs == 1 (periodic x wraps onto itself)
+ *  NCCL   one slab per process/GPU, ncclSend/ncclRecv over NVLink
+ *  LOCAL  local_slabs slabs on this one device, copies between them (the
+ *         multi-GPU data path emulated on one GPU, for tests) */
+typedef enum { LBM_COMM_NONE = 0, LBM_COMM_NCCL = 1, LBM_COMM_LOCAL = 2 } lbm_comm;
+
+typedef struct {
+    int struct_size;     /* sizeof(lbm_opts), for forward compatibility */
+    int bc;              /* lbm_bc */
+    int device;          /* CUDA device ordinal; -1 = the current device */
+    int rank, world;     /* X-slab partition: this process is slab `rank` of `world` */
+    int comm;            /* lbm_comm */
+    const void *nccl_id; /* 128-byte ncclUniqueId (same on all ranks) when comm == NCCL */
+    void *stream;        /* cudaStream_t to run on, or NULL: the context creates one */
+    int kernel;          /* lbm_kernel */
+    int local_slabs;     /* comm == LOCAL: number of slabs emulated on this device */
+} lbm_opts;
+
+/* Fills *opts with defaults: CAVITY, device -1, rank 0, world 1, NONE,
+ * no id, own stream, AUTO, 1 local slab. */
+void lbm_default_opts(lbm_opts *opts);
+
+/* Create a lattice of nx*ny*nz cells with BGK relaxation time tau
+ * (omega = 1/tau; PAPER.md delegates the collision to Palabos, PAPER.md:831,
+ * BASELINE.json fixes BGK, R-1) and lid velocity u_lid[3] (may be
+ * NULL = 0).  dtype is the storage and arithmetic type of the populations.
+ * EINVAL: nx, ny, nz < 1; tau <= 0.5 or not finite; u_lid[2] != 0 or
+ * |u_lid| > 0.3; nx % world != 0; slabs of fewer
+ * than 4 planes when world * local_slabs > 1; periodic with nx_local < 2;
+ * rank outside [0, world); comm inconsistent with world / local_slabs.
+ * The state is undefined until lbm_init_equilibrium / lbm_set_populations. */
+lbm_status lbm_create(lbm_ctx **out, int nx, int ny, int nz, double tau,
+                      const double u_lid[3], lbm_dtype dtype);
+lbm_status lbm_create_ex(lbm_ctx **out, int nx, int ny, int nz, double tau,
+                         const double u_lid[3], lbm_dtype dtype, const lbm_opts *opts);
+
+/* f_i = feq_i(rho, u) on every cell of the slab (SPEC.md:74-82 with the
+ * rest-population closure, R-2).  rho: host [nx_local][ny][nz]
+ * or NULL (= 1); u: host [nx_local][ny][nz][3] or NULL (= 0).
+ * EINVAL if any rho <= 0 or any value is not finite. */
+lbm_status lbm_init_equilibrium(lbm_ctx *ctx, const double *rho, const double *u);
+/* Same with DEVICE pointers on the context's device (not validated). */
+lbm_status lbm_init_equilibrium_device(lbm_ctx *ctx, const double *d_rho, const double *d_u);
+
+/* Advance n >= 0 time steps (asynchronous on the context stream).  Each
+ * step is collide (BGK) then stream with the boundary rules (Alg. 1,
+ * PAPER.md:275-294); pairs of steps run as one two-step sweep (Alg. 2's
+ * merge).  lbm_step(a); lbm_step(b) is bitwise identical
+ * to lbm_step(a + b).  EINVAL if n < 0; ESTATE before initialisation. */
+lbm_status lbm_step(lbm_ctx *ctx, long n);
+
+/* Moments of the canonical f(t): rho = sum_i f_i, u = (sum_i c_i f_i)/rho
+ * (the paper's velocity norms).  Host arrays
+ * rho [nx_local][ny][nz], u [nx_local][ny][nz][3]; either may be NULL.
+ * Blocks until the copy is complete. */
+lbm_status lbm_macroscopic(lbm_ctx *ctx, double *rho, double *u);
+/* Same into DEVICE arrays; asynchronous on the context stream. */
+lbm_status lbm_macroscopic_device(lbm_ctx *ctx, double *d_rho, double *d_u);
+
+/* Canonical populations f(t) as host f[19][nx_local][ny][nz] (canonical
+ * direction order).  Blocks. */
+lbm_status lbm_get_populations(lbm_ctx *ctx, double *f);
+/* The box [x0,x0+lx) x [y0,y0+ly) x [z0,z0+lz) of the slab (slab-local x)
+ * as host f[19][lx][ly][lz].  EINVAL if the box leaves the slab. */
+lbm_status lbm_get_populations_box(lbm_ctx *ctx, int x0, int y0, int z0, int lx,
+                                   int ly, int lz, double *f);
+/* Set the canonical state f(t) from host f[19][nx_local][ny][nz].  EINVAL if
+ * a value is not finite. */
+lbm_status lbm_set_populations(lbm_ctx *ctx, const double *f);
+
+/* Wait for all work queued on the context stream; reports async errors. */
+lbm_status lbm_synchronize(lbm_ctx *ctx);
+
+/* Time steps advanced since the last init / set (the canonical t - t0). */
+lbm_status lbm_get_time(const lbm_ctx *ctx, long *t);
+
+/* rank 0 creates the NCCL id that every rank passes as opts.nccl_id.
+ * out128 must hold 128 bytes.  ENCCL if libnccl.so.2 cannot be loaded. */
+lbm_status lbm_nccl_unique_id(void *out128);
+
+/* Halo plan of one X-slab, computed on the host (no GPU needed).  Offsets
+ * and counts are in ELEMENTS of the slab buffer (dtype-sized), which is
+ * laid out as planes p = 0 .. nx_local+3 (slab-local x = p - 2, two ghost
+ * planes per side), each plane [19 internal directions][ny][nz_pitch]
+ * (DESIGN.md "Data layout").  A neighbour of -1 means a wall (no exchange). */
+typedef struct {
+    int nx_local, x0;
+    int nz_pitch;            /* z row pitch in elements */
+    long long plane_q;       /* elements per (x, direction) plane = ny * nz_pitch */
+    long long plane_x;       /* elements per x plane = 19 * plane_q */
+    long long buffer_elems;  /* (nx_local + 4) * plane_x */
+    int left, right;         /* neighbour ranks or -1 */
+    long long send_left_off, send_right_off, recv_left_off, recv_right_off;
+    long long span;          /* elements per message (24 * plane_q) */
+    int dir_of_slot[19];     /* canonical direction stored at internal slot k */
+} lbm_halo_plan;
+
+lbm_status lbm_plan_halo(int nx, int ny, int nz, lbm_dtype dtype, int bc, int rank,
+                         int world, lbm_halo_plan *plan);
+
+/* Diagnostics for the bench harness (no effect on results).
+ * Kernel launches issued by this context since creation, and optional CUDA
+ * event timing of every sweep launch (K1 and K2 only) on the context
+ * stream: total milliseconds, launch count and the lattice updates they
+ * performed. */
+typedef struct {
+    long long launches;        /* all kernel launches by this context */
+    long long sweep_launches;  /* timed K1/K2 launches since lbm_profile_reset */
+    double sweep_ms;           /* their summed event time */
+    long long sweep_updates;   /* cell updates they performed */
+    long long k2_launches, k1_launches;
+} lbm_stats;
+
+lbm_status lbm_profile_enable(lbm_ctx *ctx, int on);
+lbm_status lbm_profile_reset(lbm_ctx *ctx);
+lbm_status lbm_get_stats(lbm_ctx *ctx, lbm_stats *stats); /* synchronises */
+
+/* Last error message of ctx, or of the calling thread when ctx is NULL. */
+const char *lbm_last_error(const lbm_ctx *ctx);
+
+/* Release everything the context owns.  NULL-safe. */
+void lbm_destroy(lbm_ctx *ctx);
+
+int lbm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,768 @@
+// api.cu -- the C-ABI (include/lbm.h): validation, context, X-slab engine,
+// halo exchange (local copies or NCCL send/recv), host transfers.
+//
+// Engine.  The process owns one slab (NCCL, one GPU per rank) or several
+// slabs on one device (LOCAL, the multi-GPU data path emulated on one GPU).
+// Each slab holds two buffers of post-collision populations (ping-pong) with
+// two ghost planes per side.  lbm_step(n) runs floor(n/2) two-step sweeps
+// (K2; Alg. 2's merge) and one one-step sweep (K1) if n
+// is odd, with one halo exchange before every sweep -- the analogue of
+// "we only synchronize at the intersection layers every two time steps"
+// (PAPER.md:747-749).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <nccl.h>
+
+#include "../../include/lbm.h"
+#include "kernels.h"
+
+using namespace lbm;
+
+// ------------------------------------------------------------- NCCL ------
+// libnccl.so.2 is loaded on demand (torch's copy when torch is imported
+// first); the library has no link-time NCCL dependency.
+namespace {
+struct NcclApi {
+    bool tried = false, ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool nccl_load() {
+    if (g_nccl.tried) return g_nccl.ok;
+    g_nccl.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+#define LOADSYM(field, name) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name))
+    LOADSYM(GetUniqueId, "ncclGetUniqueId");
+    LOADSYM(CommInitRank, "ncclCommInitRank");
+    LOADSYM(CommDestroy, "ncclCommDestroy");
+    LOADSYM(GroupStart, "ncclGroupStart");
+    LOADSYM(GroupEnd, "ncclGroupEnd");
+    LOADSYM(Send, "ncclSend");
+    LOADSYM(Recv, "ncclRecv");
+    LOADSYM(GetErrorString, "ncclGetErrorString");
+#undef LOADSYM
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.GroupStart &&
+                g_nccl.GroupEnd && g_nccl.Send && g_nccl.Recv;
+    return g_nccl.ok;
+}
+
+thread_local std::string t_last_error;
+}  // namespace
+
+// ------------------------------------------------------------- context ---
+struct Slab {
+    SlabGeom g;
+    void* buf[2] = {nullptr, nullptr};
+    int left = -1, right = -1;  // neighbour slab index (LOCAL/NONE) or rank (NCCL); -1 = wall
+    lbm_halo_plan plan;
+};
+
+struct lbm_ctx {
+    int nx, ny, nz;
+    double tau, ulid[3];
+    lbm_dtype dt;
+    lbm_opts opts;
+    int device = 0;
+    int nxl_proc = 0, x0_proc = 0;  // the planes this process owns (union of its slabs)
+    std::vector<Slab> slabs;
+    int cur = 0;
+    bool initialized = false, ghosts_valid = false, poisoned = false;
+    long t = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    size_t esize = 8;
+    int* d_flag = nullptr;
+    // diagnostics
+    long long launches = 0, k1_launches = 0, k2_launches = 0;
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+    std::vector<long long> event_updates;
+    size_t events_used = 0;
+    std::string err;
+};
+
+namespace {
+
+lbm_status fail(lbm_ctx* c, lbm_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_last_error = buf;
+    if (c) {
+        c->err = buf;
+        if (st == LBM_ECUDA || st == LBM_ENCCL) c->poisoned = true;
+    }
+    return st;
+}
+
+#define CK(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(c, LBM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                                  \
+    } while (0)
+
+#define CKN(call)                                                                                        \
+    do {                                                                                                 \
+        ncclResult_t r_ = (call);                                                                        \
+        if (r_ != ncclSuccess)                                                                           \
+            return fail(c, LBM_ENCCL, "%s failed: %s", #call,                                            \
+                        g_nccl.GetErrorString ? g_nccl.GetErrorString(r_) : "nccl error");               \
+    } while (0)
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world, int nxl, int x0,
+               lbm_halo_plan* p) {
+    memset(p, 0, sizeof *p);
+    p->nx_local = nxl;
+    p->x0 = x0;
+    p->nz_pitch = round_up(nz, int(32 / esize));  // rows start on 32 B sectors
+    p->plane_q = (long long)ny * p->nz_pitch;
+    p->plane_x = (long long)kQ * p->plane_q;
+    p->buffer_elems = (long long)(nxl + 4) * p->plane_x;
+    if (bc == LBM_BC_PERIODIC) {
+        p->left = (rank - 1 + world) % world;
+        p->right = (rank + 1) % world;
+    } else {
+        p->left = rank > 0 ? rank - 1 : -1;
+        p->right = rank < world - 1 ? rank + 1 : -1;
+    }
+    const long long px = p->plane_x, pq = p->plane_q;
+    // planes p = x + 2.  Left ghost: [plane 0 (x=-2): P slots | plane 1 (x=-1): all]
+    p->recv_left_off = 0 * px + kSlotP0 * pq;
+    // right ghost: [plane nxl+2 (x=nxl): all | plane nxl+3 (x=nxl+1): M slots]
+    p->recv_right_off = (long long)(nxl + 2) * px;
+    // to the left neighbour's right ghost: [x=0: all | x=1: M slots]
+    p->send_left_off = 2 * px;
+    // to the right neighbour's left ghost: [x=nxl-2: P slots | x=nxl-1: all]
+    p->send_right_off = (long long)nxl * px + kSlotP0 * pq;
+    p->span = (long long)kHaloSlots * pq;
+    for (int k = 0; k < kQ; ++k) p->dir_of_slot[k] = slot_dir(k);
+}
+
+bool finite_vec(const double* v) {
+    return v == nullptr || (std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]));
+}
+
+template <typename T>
+StepParams<T> make_params(const lbm_ctx* c, const Slab& s) {
+    StepParams<T> P;
+    P.g = s.g;
+    P.omega = T(1.0 / c->tau);
+    const double rho_w = 1.0;
+    // 6 w_i rho_w (c_i . u_lid) per slot
+    for (int k = 0; k < kQ; ++k) {
+        const int i = slot_dir(k);
+        const double w = (i == 0) ? 1.0 / 3.0 : (can_axis(i) ? 1.0 / 18.0 : 1.0 / 36.0);
+        const double cu = can_cx(i) * c->ulid[0] + can_cy(i) * c->ulid[1] + can_cz(i) * c->ulid[2];
+        P.lid[k] = T(6.0 * w * rho_w * cu);
+    }
+    return P;
+}
+
+// ---------------------------------------------------------------- halo --
+lbm_status exchange(lbm_ctx* c, int which) {
+    if (c->opts.comm == LBM_COMM_NCCL) {
+        Slab& s = c->slabs[0];
+        char* b = static_cast<char*>(s.buf[which]);
+        const size_t es = c->esize;
+        const ncclDataType_t ty = c->dt == LBM_F64 ? ncclFloat64 : ncclFloat32;
+        const size_t n = size_t(s.plan.span);
+        CKN(g_nccl.GroupStart());
+        // order: [send left, recv right], [send right, recv left]: pairs match
+        // even when left == right (a ring of two)
+        if (s.left >= 0) CKN(g_nccl.Send(b + s.plan.send_left_off * es, n, ty, s.left, c->comm, c->stream));
+        if (s.right >= 0) CKN(g_nccl.Recv(b + s.plan.recv_right_off * es, n, ty, s.right, c->comm, c->stream));
+        if (s.right >= 0) CKN(g_nccl.Send(b + s.plan.send_right_off * es, n, ty, s.right, c->comm, c->stream));
+        if (s.left >= 0) CKN(g_nccl.Recv(b + s.plan.recv_left_off * es, n, ty, s.left, c->comm, c->stream));
+        CKN(g_nccl.GroupEnd());
+    } else {
+        for (Slab& s : c->slabs) {
+            char* dst = static_cast<char*>(s.buf[which]);
+            const size_t bytes = size_t(s.plan.span) * c->esize;
+            if (s.left >= 0) {
+                const Slab& L = c->slabs[s.left];
+                const char* src = static_cast<const char*>(L.buf[which]);
+                CK(cudaMemcpyAsync(dst + s.plan.recv_left_off * c->esize, src + L.plan.send_right_off * c->esize,
+                                   bytes, cudaMemcpyDeviceToDevice, c->stream));
+            }
+            if (s.right >= 0) {
+                const Slab& R = c->slabs[s.right];
+                const char* src = static_cast<const char*>(R.buf[which]);
+                CK(cudaMemcpyAsync(dst + s.plan.recv_right_off * c->esize, src + R.plan.send_left_off * c->esize,
+                                   bytes, cudaMemcpyDeviceToDevice, c->stream));
+            }
+        }
+    }
+    return LBM_OK;
+}
+
+bool has_neighbours(const lbm_ctx* c) {
+    for (const Slab& s : c->slabs)
+        if (s.left >= 0 || s.right >= 0) return true;
+    return false;
+}
+
+lbm_status ensure_ghosts(lbm_ctx* c) {
+    if (c->ghosts_valid || !has_neighbours(c)) {
+        c->ghosts_valid = true;
+        return LBM_OK;
+    }
+    lbm_status st = exchange(c, c->cur);
+    if (st == LBM_OK) c->ghosts_valid = true;
+    return st;
+}
+
+lbm_status entry(lbm_ctx* c, bool need_init) {
+    if (!c) return fail(nullptr, LBM_EINVAL, "null context");
+    if (c->poisoned) return fail(c, LBM_ESTATE, "context poisoned by an earlier CUDA/NCCL error: %s", c->err.c_str());
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return fail(c, LBM_ECUDA, "cudaSetDevice(%d): %s", c->device, cudaGetErrorString(e));
+    if (need_init && !c->initialized)
+        return fail(c, LBM_ESTATE, "state not initialised (call lbm_init_equilibrium or lbm_set_populations)");
+    return LBM_OK;
+}
+
+// ------------------------------------------------------------ profiling --
+lbm_status prof_begin(lbm_ctx* c, size_t& slot) {
+    if (!c->profiling) return LBM_OK;
+    if (c->events_used == c->events.size()) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        c->events.push_back({a, b});
+        c->event_updates.push_back(0);
+    }
+    slot = c->events_used++;
+    CK(cudaEventRecord(c->events[slot].first, c->stream));
+    return LBM_OK;
+}
+
+lbm_status prof_end(lbm_ctx* c, size_t slot, long long updates) {
+    if (!c->profiling) return LBM_OK;
+    CK(cudaEventRecord(c->events[slot].second, c->stream));
+    c->event_updates[slot] = updates;
+    return LBM_OK;
+}
+
+// --------------------------------------------------------------- engine --
+template <typename T>
+lbm_status run_steps(lbm_ctx* c, long n) {
+    bool use_k2 = c->opts.kernel != LBM_KERNEL_K1;
+    for (const Slab& s : c->slabs) use_k2 = use_k2 && k2_supported<T>(s.g);
+    if (c->opts.kernel == LBM_KERNEL_K2 && !use_k2 && n >= 2)
+        return fail(c, LBM_EINVAL, "K2 requested but not supported for this geometry");
+    while (n > 0) {
+        const int nsteps = (use_k2 && n >= 2) ? 2 : 1;
+        if (!c->ghosts_valid && has_neighbours(c)) {
+            lbm_status st = exchange(c, c->cur);
+            if (st != LBM_OK) return st;
+        }
+        for (Slab& s : c->slabs) {
+            const StepParams<T> P = make_params<T>(c, s);
+            const T* A = static_cast<const T*>(s.buf[c->cur]);
+            T* B = static_cast<T*>(s.buf[c->cur ^ 1]);
+            size_t slot = 0;
+            lbm_status st = prof_begin(c, slot);
+            if (st != LBM_OK) return st;
+            cudaError_t e = nsteps == 2 ? launch_k2<T>(A, B, P, 0, s.g.nxl, c->stream)
+                                        : launch_k1<T>(A, B, P, 0, s.g.nxl, c->stream);
+            if (e != cudaSuccess)
+                return fail(c, LBM_ECUDA, "sweep launch failed: %s", cudaGetErrorString(e));
+            c->launches++;
+            (nsteps == 2 ? c->k2_launches : c->k1_launches)++;
+            st = prof_end(c, slot, (long long)nsteps * s.g.nxl * s.g.ny * s.g.nz);
+            if (st != LBM_OK) return st;
+        }
+        c->cur ^= 1;
+        c->ghosts_valid = false;
+        c->t += nsteps;
+        n -= nsteps;
+    }
+    return LBM_OK;
+}
+
+// validation of staged doubles on the device: flag bit 0 = non-finite, bit 1 = rho <= 0
+__global__ void k_validate(const double* __restrict__ v, long long n, int positive, int* flag) {
+    int bad = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double a = v[i];
+        if (!isfinite(a)) bad |= 1;
+        if (positive && !(a > 0.0)) bad |= 2;
+    }
+    if (bad) atomicOr(flag, bad);
+}
+
+lbm_status validate_device(lbm_ctx* c, const double* v, long long n, bool positive, int* out) {
+    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    if (n > 0) {
+        k_validate<<<592, 256, 0, c->stream>>>(v, n, positive ? 1 : 0, c->d_flag);
+        CK(cudaGetLastError());
+        c->launches++;
+    }
+    CK(cudaMemcpyAsync(out, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return LBM_OK;
+}
+
+// f(t0) canonical in buffer `which` of every slab (own planes) -> state.
+template <typename T>
+lbm_status finish_init(lbm_ctx* c, int canon) {
+    // the inverse stream reads the neighbours' canonical planes
+    if (has_neighbours(c)) {
+        lbm_status st = exchange(c, canon);
+        if (st != LBM_OK) return st;
+    }
+    for (Slab& s : c->slabs) {
+        const StepParams<T> P = make_params<T>(c, s);
+        CK(launch_k0_unstream<T>(static_cast<const T*>(s.buf[canon]), static_cast<T*>(s.buf[canon ^ 1]), P,
+                                 c->stream));
+        c->launches++;
+    }
+    c->cur = canon ^ 1;
+    c->ghosts_valid = false;
+    c->initialized = true;
+    c->t = 0;
+    return LBM_OK;
+}
+
+template <typename T>
+lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
+    const long long plane = (long long)c->ny * c->nz;
+    const int canon = c->cur;  // canonical f(t0) is built here, the state ends in the other buffer
+    for (Slab& s : c->slabs) {
+        const long long cells = (long long)s.g.nxl * plane;
+        const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;
+        const double* dr = nullptr;
+        const double* du = nullptr;
+        if (host) {
+            // stage rho, u as doubles in the slab's scratch buffer (>= 32 B per cell)
+            double* stage = static_cast<double*>(s.buf[canon ^ 1]);
+            if (rho) {
+                CK(cudaMemcpyAsync(stage, rho + xoff, cells * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+                dr = stage;
+            }
+            if (u) {
+                CK(cudaMemcpyAsync(stage + cells, u + 3 * xoff, 3 * cells * sizeof(double), cudaMemcpyHostToDevice,
+                                   c->stream));
+                du = stage + cells;
+            }
+            int flag = 0;
+            lbm_status st;
+            if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
+            if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+            if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
+            if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+        } else {
+            dr = rho ? rho + xoff : nullptr;
+            du = u ? u + 3 * xoff : nullptr;
+        }
+        CK(launch_k0_equilibrium<T>(dr, du, static_cast<T*>(s.buf[canon]), s.g, c->stream));
+        c->launches++;
+    }
+    return finish_init<T>(c, canon);
+}
+
+template <typename T>
+lbm_status set_pops(lbm_ctx* c, const double* f) {
+    const long long plane = (long long)c->ny * c->nz;
+    const long long proc_cells = (long long)c->nxl_proc * plane;
+    const int canon = c->cur ^ 1;  // import into the non-state buffer, stage in the state buffer
+    c->initialized = false;       // the state buffer is used as staging
+    for (Slab& s : c->slabs) {
+        double* stage = static_cast<double*>(s.buf[canon ^ 1]);
+        const long long cap_planes = (long long)(s.plan.buffer_elems * c->esize) / (kQ * plane * sizeof(double));
+        for (int xb = 0; xb < s.g.nxl; xb += int(cap_planes)) {
+            const int nxc = int(std::min<long long>(cap_planes, s.g.nxl - xb));
+            const long long ccells = (long long)nxc * plane;
+            const double* src = f + (long long)(s.g.x0 - c->x0_proc + xb) * plane;
+            CK(cudaMemcpy2DAsync(stage, ccells * sizeof(double), src, proc_cells * sizeof(double),
+                                 ccells * sizeof(double), kQ, cudaMemcpyHostToDevice, c->stream));
+            int flag = 0;
+            lbm_status st = validate_device(c, stage, kQ * ccells, false, &flag);
+            if (st != LBM_OK) return st;
+            if (flag) return fail(c, LBM_EINVAL, "populations must be finite (state is now undefined)");
+            CK(launch_k0_import<T>(stage, static_cast<T*>(s.buf[canon]), s.g, xb, nxc, c->stream));
+            c->launches++;
+        }
+    }
+    return finish_init<T>(c, canon);
+}
+
+template <typename T>
+lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
+    lbm_status st = ensure_ghosts(c);
+    if (st != LBM_OK) return st;
+    const long long plane = (long long)c->ny * c->nz;
+    for (Slab& s : c->slabs) {
+        const StepParams<T> P = make_params<T>(c, s);
+        const long long cells = (long long)s.g.nxl * plane;
+        const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;
+        const T* A = static_cast<const T*>(s.buf[c->cur]);
+        if (host) {
+            double* stage = static_cast<double*>(s.buf[c->cur ^ 1]);
+            CK(launch_k3_moments<T>(A, P, 0, s.g.nxl, rho ? stage : nullptr, u ? stage + cells : nullptr,
+                                    c->stream));
+            c->launches++;
+            if (rho)
+                CK(cudaMemcpyAsync(rho + xoff, stage, cells * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            if (u)
+                CK(cudaMemcpyAsync(u + 3 * xoff, stage + cells, 3 * cells * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        } else {
+            CK(launch_k3_moments<T>(A, P, 0, s.g.nxl, rho ? rho + xoff : nullptr, u ? u + 3 * xoff : nullptr,
+                                    c->stream));
+            c->launches++;
+        }
+    }
+    if (host) CK(cudaStreamSynchronize(c->stream));
+    return LBM_OK;
+}
+
+// box in process-local coordinates; out f[19][lx][ly][lz]
+template <typename T>
+lbm_status get_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, double* out) {
+    lbm_status st = ensure_ghosts(c);
+    if (st != LBM_OK) return st;
+    const long long bplane = (long long)ly * lz;
+    const long long bcells = (long long)lx * bplane;
+    for (Slab& s : c->slabs) {
+        const int sx0 = s.g.x0 - c->x0_proc;  // slab start in process coordinates
+        const int a = std::max(bx, sx0), b = std::min(bx + lx, sx0 + s.g.nxl);
+        if (a >= b) continue;
+        const StepParams<T> P = make_params<T>(c, s);
+        double* stage = static_cast<double*>(s.buf[c->cur ^ 1]);
+        const long long cap_planes = (long long)(s.plan.buffer_elems * c->esize) / (kQ * bplane * sizeof(double));
+        for (int xb = a; xb < b; xb += int(cap_planes)) {
+            const int nxc = int(std::min<long long>(cap_planes, b - xb));
+            const long long ccells = (long long)nxc * bplane;
+            CK(launch_k3_materialize<T>(static_cast<const T*>(s.buf[c->cur]), P, xb - sx0, by, bz, nxc, ly, lz, stage,
+                                        c->stream));
+            c->launches++;
+            CK(cudaMemcpy2DAsync(out + (long long)(xb - bx) * bplane, bcells * sizeof(double), stage,
+                                 ccells * sizeof(double), ccells * sizeof(double), kQ, cudaMemcpyDeviceToHost,
+                                 c->stream));
+        }
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return LBM_OK;
+}
+
+}  // namespace
+
+// ================================================================ ABI ====
+extern "C" {
+
+int lbm_abi_version(void) { return LBM_ABI_VERSION; }
+
+void lbm_default_opts(lbm_opts* o) {
+    if (!o) return;
+    memset(o, 0, sizeof *o);
+    o->struct_size = sizeof(lbm_opts);
+    o->bc = LBM_BC_CAVITY;
+    o->device = -1;
+    o->rank = 0;
+    o->world = 1;
+    o->comm = LBM_COMM_NONE;
+    o->nccl_id = nullptr;
+    o->stream = nullptr;
+    o->kernel = LBM_KERNEL_AUTO;
+    o->local_slabs = 1;
+}
+
+const char* lbm_last_error(const lbm_ctx* c) { return c ? c->err.c_str() : t_last_error.c_str(); }
+
+lbm_status lbm_plan_halo(int nx, int ny, int nz, lbm_dtype dt, int bc, int rank, int world, lbm_halo_plan* plan) {
+    lbm_ctx* c = nullptr;
+    if (!plan) return fail(c, LBM_EINVAL, "plan is NULL");
+    if (nx < 1 || ny < 1 || nz < 1) return fail(c, LBM_EINVAL, "dimensions must be >= 1");
+    if (dt != LBM_F64 && dt != LBM_F32) return fail(c, LBM_EINVAL, "bad dtype");
+    if (bc != LBM_BC_CAVITY && bc != LBM_BC_PERIODIC) return fail(c, LBM_EINVAL, "bad bc");
+    if (world < 1 || rank < 0 || rank >= world) return fail(c, LBM_EINVAL, "rank %d / world %d", rank, world);
+    if (nx % world) return fail(c, LBM_EINVAL, "nx %% world != 0");
+    const int nxl = nx / world;
+    fill_plan(nx, ny, nz, dt == LBM_F64 ? 8 : 4, bc, rank, world, nxl, rank * nxl, plan);
+    return LBM_OK;
+}
+
+lbm_status lbm_create(lbm_ctx** out, int nx, int ny, int nz, double tau, const double u_lid[3], lbm_dtype dt) {
+    return lbm_create_ex(out, nx, ny, nz, tau, u_lid, dt, nullptr);
+}
+
+lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, const double u_lid[3], lbm_dtype dt,
+                         const lbm_opts* user_opts) {
+    lbm_ctx* c = nullptr;
+    if (!out) return fail(c, LBM_EINVAL, "out is NULL");
+    *out = nullptr;
+    lbm_opts o;
+    lbm_default_opts(&o);
+    if (user_opts) {
+        if (user_opts->struct_size < int(sizeof(lbm_opts)))
+            return fail(c, LBM_EINVAL, "opts.struct_size %d < %zu", user_opts->struct_size, sizeof(lbm_opts));
+        o = *user_opts;
+    }
+    // ---- validation before any allocation ----
+    if (nx < 1 || ny < 1 || nz < 1) return fail(c, LBM_EINVAL, "dimensions must be >= 1 (got %d %d %d)", nx, ny, nz);
+    if ((long long)nx * ny * nz > (1LL << 40)) return fail(c, LBM_EINVAL, "domain too large");
+    if (!(tau > 0.5) || !std::isfinite(tau)) return fail(c, LBM_EINVAL, "tau must be finite and > 0.5 (got %g)", tau);
+    if (dt != LBM_F64 && dt != LBM_F32) return fail(c, LBM_EINVAL, "bad dtype %d", int(dt));
+    if (o.bc != LBM_BC_CAVITY && o.bc != LBM_BC_PERIODIC) return fail(c, LBM_EINVAL, "bad bc %d", o.bc);
+    if (!finite_vec(u_lid)) return fail(c, LBM_EINVAL, "u_lid must be finite");
+    double ul[3] = {0, 0, 0};
+    if (u_lid && o.bc == LBM_BC_CAVITY) memcpy(ul, u_lid, sizeof ul);
+    if (ul[2] != 0.0) return fail(c, LBM_EINVAL, "u_lid must be tangential to the z = nz-1 lid (u_lid[2] == 0)");
+    if (std::sqrt(ul[0] * ul[0] + ul[1] * ul[1]) > 0.3) return fail(c, LBM_EINVAL, "|u_lid| > 0.3");
+    if (o.world < 1 || o.rank < 0 || o.rank >= o.world)
+        return fail(c, LBM_EINVAL, "rank %d outside world %d", o.rank, o.world);
+    if (o.local_slabs < 1) return fail(c, LBM_EINVAL, "local_slabs must be >= 1");
+    if (o.comm == LBM_COMM_NONE && (o.world != 1 || o.local_slabs != 1))
+        return fail(c, LBM_EINVAL, "comm NONE needs world == 1 and local_slabs == 1");
+    if (o.comm == LBM_COMM_NCCL && (o.local_slabs != 1 || !o.nccl_id))
+        return fail(c, LBM_EINVAL, "comm NCCL needs local_slabs == 1 and an nccl_id");
+    if (o.comm == LBM_COMM_LOCAL && o.world != 1) return fail(c, LBM_EINVAL, "comm LOCAL needs world == 1");
+    if (o.comm < LBM_COMM_NONE || o.comm > LBM_COMM_LOCAL) return fail(c, LBM_EINVAL, "bad comm %d", o.comm);
+    if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K2) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    const int nslab_total = o.world * o.local_slabs;
+    if (nx % nslab_total) return fail(c, LBM_EINVAL, "nx %d not divisible by %d slabs", nx, nslab_total);
+    const int nxl = nx / nslab_total;
+    if (nslab_total > 1 && nxl < 4) return fail(c, LBM_EINVAL, "slabs need >= 4 planes (got %d)", nxl);
+    if (o.bc == LBM_BC_PERIODIC && nxl < 2) return fail(c, LBM_EINVAL, "periodic slabs need >= 2 planes");
+
+    c = new lbm_ctx();
+    c->nx = nx;
+    c->ny = ny;
+    c->nz = nz;
+    c->tau = tau;
+    memcpy(c->ulid, ul, sizeof ul);
+    c->dt = dt;
+    c->opts = o;
+    c->esize = dt == LBM_F64 ? 8 : 4;
+    if (o.device >= 0) {
+        c->device = o.device;
+    } else if (cudaGetDevice(&c->device) != cudaSuccess) {
+        lbm_status st = fail(c, LBM_ECUDA, "no CUDA device");
+        t_last_error = c->err;
+        delete c;
+        return st;
+    }
+    auto bail = [&](lbm_status st) {
+        t_last_error = c->err;
+        lbm_destroy(c);
+        return st;
+    };
+    if (cudaSetDevice(c->device) != cudaSuccess) return bail(fail(c, LBM_ECUDA, "cudaSetDevice(%d)", c->device));
+    c->nxl_proc = nx / o.world;
+    c->x0_proc = o.rank * c->nxl_proc;
+    const int sw = o.local_slabs;
+    c->slabs.resize(sw);
+    for (int j = 0; j < sw; ++j) {
+        Slab& s = c->slabs[j];
+        const int grank = o.rank * sw + j;  // global slab index
+        fill_plan(nx, ny, nz, c->esize, o.bc, grank, nslab_total, nxl, grank * nxl, &s.plan);
+        s.g.nx = nx;
+        s.g.ny = ny;
+        s.g.nz = nz;
+        s.g.nxl = nxl;
+        s.g.x0 = grank * nxl;
+        s.g.nzp = s.plan.nz_pitch;
+        s.g.pq = s.plan.plane_q;
+        s.g.px = s.plan.plane_x;
+        s.g.bc = o.bc;
+        // cavity chain: only the outer faces of the first and last slab are walls
+        s.g.left_wall = (o.bc == LBM_BC_CAVITY && grank == 0);
+        s.g.right_wall = (o.bc == LBM_BC_CAVITY && grank == nslab_total - 1);
+        if (o.comm == LBM_COMM_NCCL) {
+            s.left = s.plan.left;
+            s.right = s.plan.right;
+        } else {
+            // neighbours are local slab indices (a ring of the local slabs when periodic)
+            s.left = s.plan.left >= 0 ? s.plan.left - o.rank * sw : -1;
+            s.right = s.plan.right >= 0 ? s.plan.right - o.rank * sw : -1;
+        }
+        const size_t bytes = size_t(s.plan.buffer_elems) * c->esize;
+        for (int b = 0; b < 2; ++b) {
+            cudaError_t e = cudaMalloc(&s.buf[b], bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return bail(fail(c, LBM_ENOMEM, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e)));
+            }
+            // ghosts of wall sides are never read; zero everything once for determinism
+            if (cudaMemset(s.buf[b], 0, bytes) != cudaSuccess) return bail(fail(c, LBM_ECUDA, "cudaMemset"));
+        }
+    }
+    if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess) return bail(fail(c, LBM_ENOMEM, "cudaMalloc flag"));
+    if (o.stream) {
+        c->stream = static_cast<cudaStream_t>(o.stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(c, LBM_ECUDA, "cudaStreamCreate"));
+        c->own_stream = true;
+    }
+    if (o.comm == LBM_COMM_NCCL) {
+        if (!nccl_load()) return bail(fail(c, LBM_ENCCL, "cannot load libnccl.so.2"));
+        ncclUniqueId id;
+        memcpy(&id, o.nccl_id, sizeof id);
+        ncclResult_t r = g_nccl.CommInitRank(&c->comm, o.world, id, o.rank);
+        if (r != ncclSuccess)
+            return bail(fail(c, LBM_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(c, LBM_ECUDA, "create sync"));
+    *out = c;
+    return LBM_OK;
+}
+
+void lbm_destroy(lbm_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+    for (auto& ev : c->events) {
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    for (Slab& s : c->slabs)
+        for (void* b : s.buf)
+            if (b) cudaFree(b);
+    if (c->d_flag) cudaFree(c->d_flag);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+lbm_status lbm_init_equilibrium(lbm_ctx* c, const double* rho, const double* u) {
+    lbm_status st = entry(c, false);
+    if (st != LBM_OK) return st;
+    return c->dt == LBM_F64 ? init_eq<double>(c, rho, u, true) : init_eq<float>(c, rho, u, true);
+}
+
+lbm_status lbm_init_equilibrium_device(lbm_ctx* c, const double* rho, const double* u) {
+    lbm_status st = entry(c, false);
+    if (st != LBM_OK) return st;
+    return c->dt == LBM_F64 ? init_eq<double>(c, rho, u, false) : init_eq<float>(c, rho, u, false);
+}
+
+lbm_status lbm_set_populations(lbm_ctx* c, const double* f) {
+    lbm_status st = entry(c, false);
+    if (st != LBM_OK) return st;
+    if (!f) return fail(c, LBM_EINVAL, "f is NULL");
+    return c->dt == LBM_F64 ? set_pops<double>(c, f) : set_pops<float>(c, f);
+}
+
+lbm_status lbm_step(lbm_ctx* c, long n) {
+    if (c && n < 0) return fail(c, LBM_EINVAL, "n must be >= 0 (got %ld)", n);
+    lbm_status st = entry(c, true);
+    if (st != LBM_OK) return st;
+    return c->dt == LBM_F64 ? run_steps<double>(c, n) : run_steps<float>(c, n);
+}
+
+lbm_status lbm_macroscopic(lbm_ctx* c, double* rho, double* u) {
+    lbm_status st = entry(c, true);
+    if (st != LBM_OK) return st;
+    return c->dt == LBM_F64 ? macro<double>(c, rho, u, true) : macro<float>(c, rho, u, true);
+}
+
+lbm_status lbm_macroscopic_device(lbm_ctx* c, double* rho, double* u) {
+    lbm_status st = entry(c, true);
+    if (st != LBM_OK) return st;
+    return c->dt == LBM_F64 ? macro<double>(c, rho, u, false) : macro<float>(c, rho, u, false);
+}
+
+lbm_status lbm_get_populations_box(lbm_ctx* c, int x0, int y0, int z0, int lx, int ly, int lz, double* f) {
+    lbm_status st = entry(c, true);
+    if (st != LBM_OK) return st;
+    if (!f) return fail(c, LBM_EINVAL, "f is NULL");
+    if (lx < 0 || ly < 0 || lz < 0 || x0 < 0 || y0 < 0 || z0 < 0 || x0 + lx > c->nxl_proc || y0 + ly > c->ny ||
+        z0 + lz > c->nz)
+        return fail(c, LBM_EINVAL, "box outside the slab");
+    if ((long long)lx * ly * lz == 0) return LBM_OK;
+    return c->dt == LBM_F64 ? get_box<double>(c, x0, y0, z0, lx, ly, lz, f)
+                            : get_box<float>(c, x0, y0, z0, lx, ly, lz, f);
+}
+
+lbm_status lbm_get_populations(lbm_ctx* c, double* f) {
+    if (!c) return fail(nullptr, LBM_EINVAL, "null context");
+    return lbm_get_populations_box(c, 0, 0, 0, c->nxl_proc, c->ny, c->nz, f);
+}
+
+lbm_status lbm_synchronize(lbm_ctx* c) {
+    lbm_status st = entry(c, false);
+    if (st != LBM_OK) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    return LBM_OK;
+}
+
+lbm_status lbm_get_time(const lbm_ctx* c, long* t) {
+    if (!c || !t) return fail(nullptr, LBM_EINVAL, "null argument");
+    *t = c->t;
+    return LBM_OK;
+}
+
+lbm_status lbm_nccl_unique_id(void* out128) {
+    lbm_ctx* c = nullptr;
+    if (!out128) return fail(c, LBM_EINVAL, "out is NULL");
+    if (!nccl_load()) return fail(c, LBM_ENCCL, "cannot load libnccl.so.2");
+    ncclUniqueId id;
+    ncclResult_t r = g_nccl.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(c, LBM_ENCCL, "ncclGetUniqueId failed");
+    memcpy(out128, &id, sizeof id);
+    return LBM_OK;
+}
+
+lbm_status lbm_profile_enable(lbm_ctx* c, int on) {
+    lbm_status st = entry(c, false);
+    if (st != LBM_OK) return st;
+    c->profiling = on != 0;
+    return LBM_OK;
+}
+
+lbm_status lbm_profile_reset(lbm_ctx* c) {
+    lbm_status st = entry(c, false);
+    if (st != LBM_OK) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    c->events_used = 0;
+    return LBM_OK;
+}
+
+lbm_status lbm_get_stats(lbm_ctx* c, lbm_stats* s) {
+    lbm_status st = entry(c, false);
+    if (st != LBM_OK) return st;
+    if (!s) return fail(c, LBM_EINVAL, "stats is NULL");
+    CK(cudaStreamSynchronize(c->stream));
+    memset(s, 0, sizeof *s);
+    s->launches = c->launches;
+    s->k1_launches = c->k1_launches;
+    s->k2_launches = c->k2_launches;
+    for (size_t i = 0; i < c->events_used; ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->events[i].first, c->events[i].second));
+        s->sweep_ms += ms;
+        s->sweep_updates += c->event_updates[i];
+        s->sweep_launches++;
+    }
+    return LBM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+// kernels.cu -- K0 (init), K1 (one fused step), K3 (read-back) for sm_100a.
+//
+// Storage is "pull" form: a buffer holds the post-collision populations
+// f*(t-1) of every cell, and the canonical state is f(t) = S(f*(t-1)), S the
+// stream with the boundary rules.  One step is f*(t) = C(S(f*(t-1))): a
+// gather of 19 neighbours, the BGK collision in registers, 19 aligned
+// stores -- the paper's loop fusion of collide and stream (PAPER.md:232,
+// 236, "Fuse Swap LBM") with the in-place swap replaced by a coalesced pull
+// gather between two buffers.
+#include "kernels.h"
+
+namespace lbm {
+
+// ------------------------------------------------------------------ K1 --
+// One thread per cell; a warp covers 32 consecutive z of one row, so each of
+// the 19 loads and 19 stores of a warp is one contiguous 256 B (fp64) or
+// 128 B (fp32) segment (shifted by one element for c_z != 0 directions).
+template <typename T, int BC>
+__global__ void __launch_bounds__(256) k1_step(const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
+                                              int xbeg) {
+    const int z = blockIdx.x * 32 + threadIdx.x;
+    const int y = blockIdx.y * 8 + threadIdx.y;
+    const int x = xbeg + blockIdx.z;
+    if (z >= P.g.nz || y >= P.g.ny) return;
+    T f[kQ];
+    pull_cell<T, BC>(A, P, x, y, z, f);
+    bgk_collide<T>(f, P.omega);
+    const long long self = cell_off(P.g, x, y, z);
+    static_for<0, kQ>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        __stcs(B + self + (long long)k * P.g.pq, f[slot_dir(k)]);
+    });
+}
+
+// ------------------------------------------------------------ K0 init --
+// K0a: canonical f = feq(rho, u) of every slab cell into buffer C (slot
+// layout).  rho/u are double arrays [x][y][z] / [x][y][z][3] of the slab.
+template <typename T>
+__global__ void __launch_bounds__(256) k0_equilibrium(const double* __restrict__ rho, const double* __restrict__ u,
+                                                     T* __restrict__ C, SlabGeom g) {
+    const int z = blockIdx.x * 32 + threadIdx.x;
+    const int y = blockIdx.y * 8 + threadIdx.y;
+    const int x = blockIdx.z;
+    if (z >= g.nz || y >= g.ny) return;
+    const long long cell = ((long long)x * g.ny + y) * g.nz + z;
+    const T r = rho ? T(rho[cell]) : T(1);
+    T ux = T(0), uy = T(0), uz = T(0);
+    if (u) {
+        ux = T(u[3 * cell + 0]);
+        uy = T(u[3 * cell + 1]);
+        uz = T(u[3 * cell + 2]);
+    }
+    T feq[kQ];
+    equilibrium<T>(r, ux, uy, uz, feq);
+    const long long self = cell_off(g, x, y, z);
+    static_for<0, kQ>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        C[self + (long long)k * g.pq] = feq[slot_dir(k)];
+    });
+}
+
+// K0b: the inverse stream, f*(t-1) = S^-1(f(t)).  S is a permutation of the
+// slots plus the lid constants, so slot j at cell y takes
+//   f_j(y + c_j)                              if y + c_j is a cell (or ghost / wrap)
+//   f_opp(j)(y) - [(y + c_j)_z >= nz] lid_opp(j)  if y + c_j is beyond a wall.
+// C must have valid ghost planes.
+template <typename T, int BC>
+__global__ void __launch_bounds__(256) k0_unstream(const T* __restrict__ C, T* __restrict__ A, StepParams<T> P) {
+    const int z = blockIdx.x * 32 + threadIdx.x;
+    const int y = blockIdx.y * 8 + threadIdx.y;
+    const int x = blockIdx.z;
+    const SlabGeom& g = P.g;
+    if (z >= g.nz || y >= g.ny) return;
+    const long long self = cell_off(g, x, y, z);
+    static_for<0, kQ>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        constexpr int j = slot_dir(k);
+        constexpr int cx = can_cx(j), cy = can_cy(j), cz = can_cz(j);
+        int ty = y + cy, tz = z + cz;
+        bool wall = false;
+        if constexpr (BC == BC_CAVITY) {
+            if constexpr (cx == -1) wall = wall || (x == 0 && g.left_wall);
+            if constexpr (cx == 1) wall = wall || (x == g.nxl - 1 && g.right_wall);
+            if constexpr (cy == -1) wall = wall || (y == 0);
+            if constexpr (cy == 1) wall = wall || (y == g.ny - 1);
+            if constexpr (cz == -1) wall = wall || (z == 0);
+            if constexpr (cz == 1) wall = wall || (z == g.nz - 1);
+        } else {
+            if constexpr (cy == -1) ty = (y == 0) ? g.ny - 1 : ty;
+            if constexpr (cy == 1) ty = (y == g.ny - 1) ? 0 : ty;
+            if constexpr (cz == -1) tz = (z == 0) ? g.nz - 1 : tz;
+            if constexpr (cz == 1) tz = (z == g.nz - 1) ? 0 : tz;
+        }
+        T v;
+        if (!wall) {
+            v = C[(long long)(x + cx + 2) * g.px + (long long)k * g.pq + (long long)ty * g.nzp + tz];
+        } else {
+            constexpr int ko = slot_opp(k);
+            v = C[self + (long long)ko * g.pq];
+            if constexpr (cz == 1) {
+                if (z == g.nz - 1) v = v - P.lid[ko];
+            }
+        }
+        A[self + (long long)k * g.pq] = v;
+    });
+}
+
+// Import canonical host-order doubles f[19][nx_c][ny][nz] (a chunk of nx_c
+// planes starting at slab-local xbeg) into slot layout C.
+template <typename T>
+__global__ void __launch_bounds__(256) k0_import(const double* __restrict__ src, T* __restrict__ C, SlabGeom g,
+                                                int xbeg, int nxc) {
+    const int z = blockIdx.x * 32 + threadIdx.x;
+    const int y = blockIdx.y * 8 + threadIdx.y;
+    const int xc = blockIdx.z;
+    if (z >= g.nz || y >= g.ny) return;
+    const long long cstride = (long long)nxc * g.ny * g.nz;
+    const long long cell = ((long long)xc * g.ny + y) * g.nz + z;
+    const long long self = cell_off(g, xbeg + xc, y, z);
+    static_for<0, kQ>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        C[self + (long long)k * g.pq] = T(src[(long long)slot_dir(k) * cstride + cell]);
+    });
+}
+
+// -------------------------------------------------------- K3 read-back --
+// Canonical f(t) = S(A) on the box [x0,x0+lx) x [y0,y0+ly) x [z0,z0+lz) of
+// the slab, written as doubles out[19][lx][ly][lz].
+template <typename T, int BC>
+__global__ void __launch_bounds__(256) k3_materialize(const T* __restrict__ A, StepParams<T> P, int x0, int y0,
+                                                     int z0, int lx, int ly, int lz, double* __restrict__ out) {
+    const int zz = blockIdx.x * 32 + threadIdx.x;
+    const int yy = blockIdx.y * 8 + threadIdx.y;
+    const int xx = blockIdx.z;
+    if (zz >= lz || yy >= ly) return;
+    T f[kQ];
+    pull_cell<T, BC>(A, P, x0 + xx, y0 + yy, z0 + zz, f);
+    const long long stride = (long long)lx * ly * lz;
+    const long long cell = ((long long)xx * ly + yy) * lz + zz;
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) out[i * stride + cell] = double(f[i]);
+}
+
+// Moments of the canonical f(t) on planes [xbeg, xbeg + nxc): rho[x][y][z],
+// u[x][y][z][3] (doubles, chunk-local x).
+template <typename T, int BC>
+__global__ void __launch_bounds__(256) k3_moments(const T* __restrict__ A, StepParams<T> P, int xbeg, int nxc,
+                                                 double* __restrict__ rho, double* __restrict__ u) {
+    const int z = blockIdx.x * 32 + threadIdx.x;
+    const int y = blockIdx.y * 8 + threadIdx.y;
+    const int xc = blockIdx.z;
+    if (z >= P.g.nz || y >= P.g.ny) return;
+    T f[kQ];
+    pull_cell<T, BC>(A, P, xbeg + xc, y, z, f);
+    T r, ux, uy, uz;
+    moments<T>(f, r, ux, uy, uz);
+    const long long cell = ((long long)xc * P.g.ny + y) * P.g.nz + z;
+    if (rho) rho[cell] = double(r);
+    if (u) {
+        u[3 * cell + 0] = double(ux);
+        u[3 * cell + 1] = double(uy);
+        u[3 * cell + 2] = double(uz);
+    }
+}
+
+// ------------------------------------------------------------ launchers --
+static dim3 cell_grid(int nz, int ny, int nxs) { return dim3((nz + 31) / 32, (ny + 7) / 8, nxs); }
+static const dim3 kBlock(32, 8, 1);
+
+template <typename T>
+cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
+    if (nxs <= 0) return cudaSuccess;
+    if (P.g.bc == BC_PERIODIC)
+        k1_step<T, BC_PERIODIC><<<cell_grid(P.g.nz, P.g.ny, nxs), kBlock, 0, s>>>(A, B, P, xbeg);
+    else
+        k1_step<T, BC_CAVITY><<<cell_grid(P.g.nz, P.g.ny, nxs), kBlock, 0, s>>>(A, B, P, xbeg);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, const SlabGeom& g, cudaStream_t s) {
+    k0_equilibrium<T><<<cell_grid(g.nz, g.ny, g.nxl), kBlock, 0, s>>>(rho, u, C, g);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_k0_unstream(const T* C, T* A, const StepParams<T>& P, cudaStream_t s) {
+    if (P.g.bc == BC_PERIODIC)
+        k0_unstream<T, BC_PERIODIC><<<cell_grid(P.g.nz, P.g.ny, P.g.nxl), kBlock, 0, s>>>(C, A, P);
+    else
+        k0_unstream<T, BC_CAVITY><<<cell_grid(P.g.nz, P.g.ny, P.g.nxl), kBlock, 0, s>>>(C, A, P);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_k0_import(const double* src, T* C, const SlabGeom& g, int xbeg, int nxc, cudaStream_t s) {
+    k0_import<T><<<cell_grid(g.nz, g.ny, nxc), kBlock, 0, s>>>(src, C, g, xbeg, nxc);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_k3_materialize(const T* A, const StepParams<T>& P, int x0, int y0, int z0, int lx, int ly,
+                                  int lz, double* out, cudaStream_t s) {
+    if (P.g.bc == BC_PERIODIC)
+        k3_materialize<T, BC_PERIODIC><<<cell_grid(lz, ly, lx), kBlock, 0, s>>>(A, P, x0, y0, z0, lx, ly, lz, out);
+    else
+        k3_materialize<T, BC_CAVITY><<<cell_grid(lz, ly, lx), kBlock, 0, s>>>(A, P, x0, y0, z0, lx, ly, lz, out);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int nxc, double* rho, double* u,
+                              cudaStream_t s) {
+    if (P.g.bc == BC_PERIODIC)
+        k3_moments<T, BC_PERIODIC><<<cell_grid(P.g.nz, P.g.ny, nxc), kBlock, 0, s>>>(A, P, xbeg, nxc, rho, u);
+    else
+        k3_moments<T, BC_CAVITY><<<cell_grid(P.g.nz, P.g.ny, nxc), kBlock, 0, s>>>(A, P, xbeg, nxc, rho, u);
+    return cudaGetLastError();
+}
+
+#define LBM_INSTANTIATE(T)                                                                                   \
+    template cudaError_t launch_k1<T>(const T*, T*, const StepParams<T>&, int, int, cudaStream_t);           \
+    template cudaError_t launch_k0_equilibrium<T>(const double*, const double*, T*, const SlabGeom&,         \
+                                                  cudaStream_t);                                             \
+    template cudaError_t launch_k0_unstream<T>(const T*, T*, const StepParams<T>&, cudaStream_t);            \
+    template cudaError_t launch_k0_import<T>(const double*, T*, const SlabGeom&, int, int, cudaStream_t);    \
+    template cudaError_t launch_k3_materialize<T>(const T*, const StepParams<T>&, int, int, int, int, int,   \
+                                                  int, double*, cudaStream_t);                               \
+    template cudaError_t launch_k3_moments<T>(const T*, const StepParams<T>&, int, int, double*, double*,    \
+                                              cudaStream_t);
+LBM_INSTANTIATE(double)
+LBM_INSTANTIATE(float)
+
+}  // namespace lbm

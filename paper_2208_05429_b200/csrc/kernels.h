@@ -1,0 +1,33 @@
+// kernels.h -- host launchers of the library's kernels (internal; not ABI).
+#pragma once
+
+#include "d3q19.cuh"
+
+namespace lbm {
+
+// K1: one fused collide+stream step, A = f*(t-1) -> B = f*(t), slab-local
+// planes [xbeg, xbeg + nxs).  A's ghost planes must be valid.
+template <typename T>
+cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s);
+
+// K2: two fused steps, A = f*(t-1) -> B = f*(t+1) on planes [xbeg, xbeg+nxs).
+// A's two ghost planes per side must be valid.
+template <typename T>
+cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s);
+template <typename T>
+bool k2_supported(const SlabGeom& g);
+
+template <typename T>
+cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, const SlabGeom& g, cudaStream_t s);
+template <typename T>
+cudaError_t launch_k0_unstream(const T* C, T* A, const StepParams<T>& P, cudaStream_t s);
+template <typename T>
+cudaError_t launch_k0_import(const double* src, T* C, const SlabGeom& g, int xbeg, int nxc, cudaStream_t s);
+template <typename T>
+cudaError_t launch_k3_materialize(const T* A, const StepParams<T>& P, int x0, int y0, int z0, int lx, int ly,
+                                  int lz, double* out, cudaStream_t s);
+template <typename T>
+cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int nxc, double* rho, double* u,
+                              cudaStream_t s);
+
+}  // namespace lbm

@@ -1,0 +1,121 @@
+"""The C-ABI library without a GPU: it loads, exports every symbol that
+include/lbm.h declares, validates arguments before touching the device, and
+its host-side halo plan is consistent."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2208_05429_b200 as lbm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "lbm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lbm_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    L = ctypes.CDLL(lbm.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), f"{s} declared in include/lbm.h but not exported"
+    assert sorted(lbm.EXPORTS) == syms
+    assert lbm.lbm_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {lbm.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("args,msg", [
+    ((0, 4, 4, 0.6, None, 0), "dimensions"),
+    ((4, 4, 4, 0.5, None, 0), "tau"),
+    ((4, 4, 4, float("nan"), None, 0), "tau"),
+    ((4, 4, 4, 0.6, (0.0, 0.0, 0.1), 0), "tangential"),
+    ((4, 4, 4, 0.6, (0.4, 0.0, 0.0), 0), "0.3"),
+    ((4, 4, 4, 0.6, None, 7), "dtype"),
+])
+def test_create_rejects_before_allocation(args, msg):
+    with pytest.raises(lbm.LbmError) as e:
+        lbm.lbm_create(*args)
+    assert e.value.status == 1 and msg in str(e.value)
+
+
+def test_create_rejects_bad_partitions():
+    o = lbm.lbm_default_opts()
+    o.comm, o.local_slabs = lbm.LBM_COMM_LOCAL, 3
+    with pytest.raises(lbm.LbmError, match="divisible"):
+        lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+    o.local_slabs = 8
+    with pytest.raises(lbm.LbmError, match=">= 4 planes"):
+        lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+    o = lbm.lbm_default_opts()
+    o.world, o.rank = 2, 0
+    with pytest.raises(lbm.LbmError, match="comm NONE"):
+        lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+    o.comm = lbm.LBM_COMM_NCCL
+    with pytest.raises(lbm.LbmError, match="nccl_id"):
+        lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+    o = lbm.lbm_default_opts()
+    o.bc = lbm.LBM_BC_PERIODIC
+    with pytest.raises(lbm.LbmError, match="periodic"):
+        lbm.lbm_create_ex(1, 4, 4, 0.6, None, "f64", o)
+
+
+def test_step_rejects_negative_and_null():
+    with pytest.raises(lbm.LbmError):
+        lbm.lbm_step(None, 1)
+
+
+def test_no_gpu_reports_cuda_error_not_crash():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(lbm.LbmError) as e:
+        lbm.lbm_create(8, 8, 8, 0.6, (0.05, 0, 0), "f64")
+    assert e.value.status in (3, 2)
+
+
+@pytest.mark.parametrize("dtype,esize,pitch", [("f64", 8, 8), ("f32", 4, 8)])
+def test_halo_plan_layout(dtype, esize, pitch):
+    nx, ny, nz = 32, 6, 5
+    for world in (1, 2, 4):
+        for bc in (lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC):
+            for r in range(world):
+                p = lbm.lbm_plan_halo(nx, ny, nz, dtype, bc, r, world)
+                nxl = nx // world
+                assert p.nx_local == nxl and p.x0 == r * nxl
+                assert p.nz_pitch == pitch and (p.nz_pitch * esize) % 32 == 0
+                assert p.plane_q == ny * p.nz_pitch and p.plane_x == 19 * p.plane_q
+                assert p.buffer_elems == (nxl + 4) * p.plane_x
+                assert p.span == 24 * p.plane_q
+                # spans stay inside the buffer and the ghost spans stay inside ghost planes
+                for off in (p.send_left_off, p.send_right_off, p.recv_left_off, p.recv_right_off):
+                    assert 0 <= off and off + p.span <= p.buffer_elems
+                assert p.recv_left_off + p.span == 2 * p.plane_x
+                assert p.recv_right_off == (nxl + 2) * p.plane_x
+                assert p.send_left_off == 2 * p.plane_x
+                assert p.send_right_off + p.span == (nxl + 2) * p.plane_x
+                if bc == lbm.LBM_BC_PERIODIC:
+                    assert p.left == (r - 1) % world and p.right == (r + 1) % world
+                else:
+                    assert p.left == (r - 1 if r > 0 else -1)
+                    assert p.right == (r + 1 if r < world - 1 else -1)
+                slots = list(p.dir_of_slot)
+                assert sorted(slots) == list(range(19))
+                cx = [0, -1, 0, 0, -1, -1, -1, -1, 0, 0, 1, 0, 0, 1, 1, 1, 1, 0, 0]
+                assert [cx[i] for i in slots] == [-1] * 5 + [0] * 9 + [1] * 5
+
+
+def test_plan_rejects_bad_args():
+    with pytest.raises(lbm.LbmError):
+        lbm.lbm_plan_halo(10, 4, 4, "f64", 0, 0, 3)
+    with pytest.raises(lbm.LbmError):
+        lbm.lbm_plan_halo(8, 4, 4, "f64", 0, 2, 2)

@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on
+the same seeded inputs, element by element.  Tolerances (BASELINE.json:5,
+DESIGN.md R-11): max |f_gpu - f_oracle| / |f_oracle| <= 1e-12 (fp64),
+<= 1e-5 (fp32); bitwise equality where the arithmetic is identical (K1 vs K2,
+step splitting, slab partitions)."""
+import math
+
+import numpy as np
+import pytest
+
+import lbm_inputs as li
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no GPU", allow_module_level=True)
+
+import paper_2208_05429_b200 as lbm  # noqa: E402
+
+TOL = {"f64": 1e-12, "f32": 1e-5}
+LID = (0.05, 0.0, 0.0)
+
+
+def relerr(a, b):
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+def oracle_from_fields(cfg, n):
+    rho, u = li.init_fields(cfg)
+    f0 = oracle.init_equilibrium(cfg.nx, cfg.ny, cfg.nz, rho, u)
+    return rho, u, f0, oracle.run(f0, cfg.bc, cfg.tau, cfg.u_lid, n)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_config1_full(dtype):
+    cfg = li.CONFIGS[1]
+    rho, u, f0, ref = oracle_from_fields(cfg, cfg.steps)
+    with lbm.Lattice(cfg.nx, cfg.ny, cfg.nz, cfg.tau, cfg.u_lid, dtype, bc=cfg.bc) as lat:
+        lat.init_equilibrium(rho, u)
+        g0 = lat.populations()
+        assert relerr(g0, f0) <= TOL[dtype]
+        lat.step(cfg.steps)
+        assert lat.time == cfg.steps
+        got = lat.populations()
+        r, uu = lat.macroscopic()
+    assert relerr(got, ref) <= TOL[dtype]
+    rr, ur = oracle.macroscopic(ref)
+    assert np.max(np.abs(r - rr)) <= 10 * TOL[dtype]
+    assert np.max(np.abs(uu - ur)) <= 10 * TOL[dtype]
+
+
+@pytest.mark.parametrize("dims", [(5, 6, 7), (9, 33, 35), (4, 8, 64), (12, 17, 70)])
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_random_populations_ragged(dims, bc, dtype):
+    """Off-equilibrium random f on sizes spanning several 32-wide z tiles and
+    8-row y tiles with ragged tails; odd and even step counts."""
+    f0 = li.random_populations(21, *dims)
+    tau = 0.55
+    with lbm.Lattice(*dims, tau, LID, dtype, bc=bc) as lat:
+        lat.set_populations(f0)
+        assert relerr(lat.populations(), f0) <= TOL[dtype]
+        ref = f0
+        for n in (1, 2, 3):
+            lat.step(n)
+            ref = oracle.run(ref, bc, tau, LID, n)
+            assert relerr(lat.populations(), ref) <= TOL[dtype] * (10 if dtype == "f32" else 1)
+
+
+def test_config2_full_with_mass():
+    """BASELINE.json:8: 64^3 cavity, 1000 steps, oracle check and mass
+    conservation (relative drift <= 1e-13, BASELINE.json:5)."""
+    cfg = li.CONFIGS[2]
+    rho, u, f0, ref = oracle_from_fields(cfg, cfg.steps)
+    with lbm.Lattice(cfg.nx, cfg.ny, cfg.nz, cfg.tau, cfg.u_lid, "f64", bc=cfg.bc) as lat:
+        lat.init_equilibrium(rho, u)
+        m0 = math.fsum(lat.populations().ravel())
+        lat.step(cfg.steps)
+        got = lat.populations()
+    assert relerr(got, ref) <= 1e-12
+    assert abs(math.fsum(got.ravel()) - m0) / m0 <= 1e-13
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_kernel_choice_and_step_splitting_bitwise(dtype):
+    dims = (10, 20, 36)
+    f0 = li.random_populations(22, *dims)
+    outs = []
+    for kernel, chunks in [(lbm.LBM_KERNEL_K1, [8]), (lbm.LBM_KERNEL_AUTO, [8]), (lbm.LBM_KERNEL_AUTO, [3, 5]),
+                           (lbm.LBM_KERNEL_AUTO, [1, 1, 2, 4]), (lbm.LBM_KERNEL_K1, [7, 1])]:
+        with lbm.Lattice(*dims, 0.6, LID, dtype, kernel=kernel) as lat:
+            lat.set_populations(f0)
+            for n in chunks:
+                lat.step(n)
+            outs.append(lat.populations())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
+@pytest.mark.parametrize("slabs", [2, 4])
+def test_local_slabs_bitwise(bc, slabs):
+    """The X-slab data path (ghost planes + halo spans) emulated on one GPU:
+    G slabs give identical bits to one slab, and match the oracle."""
+    dims = (16, 12, 20)
+    f0 = li.random_populations(23, *dims)
+    with lbm.Lattice(*dims, 0.6, LID, "f64", bc=bc) as lat:
+        lat.set_populations(f0)
+        lat.step(5)
+        one = lat.populations()
+    with lbm.Lattice(*dims, 0.6, LID, "f64", bc=bc, comm=lbm.LBM_COMM_LOCAL, local_slabs=slabs) as lat:
+        lat.set_populations(f0)
+        lat.step(5)
+        many = lat.populations()
+        r, u = lat.macroscopic()
+    assert np.array_equal(one, many)
+    assert relerr(many, oracle.run(f0, bc, 0.6, LID, 5)) <= 1e-12
+
+
+def test_init_equilibrium_local_slabs():
+    cfg = li.CONFIGS[1]
+    rho, u, f0, ref = oracle_from_fields(cfg, 6)
+    with lbm.Lattice(cfg.nx, cfg.ny, cfg.nz, cfg.tau, cfg.u_lid, "f64", comm=lbm.LBM_COMM_LOCAL,
+                     local_slabs=4) as lat:
+        lat.init_equilibrium(rho, u)
+        lat.step(6)
+        assert relerr(lat.populations(), ref) <= 1e-12
+
+
+def test_box_readback_matches_full():
+    dims = (8, 10, 40)
+    f0 = li.random_populations(24, *dims)
+    with lbm.Lattice(*dims, 0.6, LID, "f64") as lat:
+        lat.set_populations(f0)
+        lat.step(3)
+        full = lat.populations()
+        box = lat.populations_box(2, 3, 5, 4, 6, 33)
+    assert np.array_equal(box, full[:, 2:6, 3:9, 5:38])
+
+
+def test_zero_steps_roundtrip_and_errors():
+    dims = (6, 6, 6)
+    f0 = li.random_populations(25, *dims)
+    with lbm.Lattice(*dims, 0.6, LID, "f64") as lat:
+        with pytest.raises(lbm.LbmError, match="not initialised"):
+            lat.step(1)
+        lat.set_populations(f0)
+        lat.step(0)
+        assert relerr(lat.populations(), f0) <= 1e-15
+        with pytest.raises(lbm.LbmError):
+            lat.step(-1)
+        bad = f0.copy()
+        bad[3, 1, 1, 1] = np.nan
+        with pytest.raises(lbm.LbmError, match="finite"):
+            lat.set_populations(bad)
+        rho = np.ones(dims)
+        rho[0, 0, 0] = -1.0
+        with pytest.raises(lbm.LbmError, match="rho"):
+            lat.init_equilibrium(rho, None)
+
+
+def test_rest_state_and_lid_closed_form():
+    nx, ny, nz = 8, 8, 8
+    with lbm.Lattice(nx, ny, nz, 0.6, LID, "f64") as lat:
+        lat.init_equilibrium(None, None)
+        lat.step(1)
+        g = lat.populations()
+    _, w, _ = oracle.d3q19()
+    assert np.allclose(g[16, :, :, nz - 1], 1 / 36 + 1 / 120, atol=4e-16, rtol=0)
+    assert np.allclose(g[6, :, :, nz - 1], 1 / 36 - 1 / 120, atol=4e-16, rtol=0)
+    with lbm.Lattice(nx, ny, nz, 0.6, (0, 0, 0), "f64") as lat:
+        lat.init_equilibrium(None, None)
+        lat.step(100)
+        g = lat.populations()
+    assert np.max(np.abs(g - w[:, None, None, None])) <= 1e-15
