@@ -174,6 +174,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "k1", "k2"])
     ap.add_argument("--lbm-steps", type=int, default=None, help="time steps per job (default: the config's)")
+    ap.add_argument("--dims", default=None, help="override NX,NY,NZ (profiling runs only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -183,6 +184,9 @@ def main():
     if args.lbm_steps is not None:
         cfg = li.Config(cfg.name, cfg.nx, cfg.ny, cfg.nz, cfg.bc, cfg.tau, cfg.u_lid, args.lbm_steps, cfg.seed,
                         cfg.init, cfg.note)
+    if args.dims:
+        nx, ny, nz = (int(v) for v in args.dims.split(","))
+        cfg = cfg.with_dims(nx, ny, nz)
     if args.impl == "reference":
         return run_reference(args, cfg)
 

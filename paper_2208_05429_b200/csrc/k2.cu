@@ -1,17 +1,398 @@
-// k2.cu -- K2, the two-step temporally blocked sweep (placeholder until the
-// TMA kernel lands; the engine falls back to K1 pairs, bitwise identical).
+// k2.cu -- K2: two collision-streaming steps per HBM pass (temporal blocking),
+// the GPU form of the paper's two-step merge (Alg. 2, PAPER.md:140-216:
+// "after a cell completes the first computation ... cell (1,1,1) is ready for
+// the second collide").
+//
+// Each CTA owns an output tile T of TY x TZ cells in the (y, z) plane and
+// marches along x over a chunk of planes (the paper's X-outermost order,
+// PAPER.md:335).  Per input plane p:
+//   1. TMA stages f(t) on the tile plus a one-cell halo T+1: one box per
+//      direction, its origin shifted by -c_i, so the TMA unit performs the
+//      pull-stream (19 cp.async.bulk.tensor per plane, one mbarrier,
+//      double-buffered, two planes in flight).  Boxes that leave the domain
+//      are patched (bounce-back + lid, or periodic wrap) by a lean fix-up pass
+//      that only edge tiles and wall planes run.
+//   2. Step 1: every cell of T+1 collides (BGK, registers) and PUSHES its
+//      post-collision populations into a destination-indexed SMEM ring:
+//      direction i goes to the cell it streams to, (p + c_x, y + c_y, z + c_z).
+//      Wall links are resolved at the same time (bounce-back + lid into the
+//      cell's own slot), so the ring holds exactly f(t+1) of the tile.
+//   3. Step 2: once plane p has pushed, plane p-1 of the ring is complete;
+//      its cells collide again and store f*(t+1) to HBM with coalesced
+//      streaming stores.
+// The ring keeps, per destination plane, only the populations still to
+// arrive: c_x = -1 group (5) x 2 planes, c_x = 0 (9) x 2, c_x = +1 (5) x 3.
+// Every population therefore crosses HBM once per two steps (plus the halo
+// re-reads, which hit L2 when neighbouring tiles march in step).
+//
+// The arithmetic is the same bgk_collide()/pull rules as K1 (d3q19.cuh), so
+// K2 == K1 o K1 bit for bit (tests/test_gpu_parity.py).
+#include <cuda.h>
+
+#include <cstdio>
+#include <mutex>
+
 #include "kernels.h"
 
 namespace lbm {
 
-template <typename T>
-bool k2_supported(const SlabGeom&) {
-    return false;
+namespace {
+
+__host__ __device__ constexpr int round_up_c(int v, int m) { return (v + m - 1) / m * m; }
+
+template <typename T, int TY_, int TZ_>
+struct K2Cfg {
+    static constexpr int TY = TY_, TZ = TZ_;
+    static constexpr int HY = TY + 2, HZ = TZ + 2;            // tile + one-cell halo
+    // The TMA box origin's innermost coordinate must be 16-byte aligned, so a
+    // box starts ZPAD elements before the tile (z0 - ZPAD, z0 a multiple of
+    // 32) and spans TZ + 2 ZPAD; the -c_z shift is applied when reading.
+    static constexpr int ZPAD = 16 / int(sizeof(T));
+    static constexpr int BW = TZ + 2 * ZPAD;
+    static constexpr int BOX = HY * BW;                        // staged elements per direction
+    static constexpr int BOXE = round_up_c(BOX * int(sizeof(T)), 128) / int(sizeof(T));  // 128 B aligned
+    static constexpr int NT = round_up_c(HY * HZ, 32);         // threads: one per T+1 cell
+    static constexpr int RP = TY * TZ;                         // ring plane (one direction)
+    static constexpr int RING = (2 * 5 + 2 * 9 + 3 * 5) * RP;  // 43 direction-planes
+    static constexpr size_t SMEM = size_t(2 * kQ * BOXE + RING) * sizeof(T) + 2 * sizeof(uint64_t);
+    static constexpr uint32_t TX_BYTES = uint32_t(kQ * BOX * sizeof(T));
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Bounded wait: a TMA that never completes traps (a kernel error the host
+// reports) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    for (uint32_t spin = 0; !mbar_try_wait(bar, parity); ++spin) {
+        if (spin > (1u << 28)) __trap();
+    }
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ int wrapi(int v, int n) {
+    v %= n;
+    return v < 0 ? v + n : v;
+}
+
+}  // namespace
+
+template <typename T, int BC, int TY, int TZ>
+__global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, 1)
+    k2_sweep(const __grid_constant__ CUtensorMap tmA, const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
+             int xbeg, int xend, int chunk) {
+    using C = K2Cfg<T, TY, TZ>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* const stage = reinterpret_cast<T*>(smem_raw);
+    T* const ringM = stage + 2 * kQ * C::BOXE;
+    T* const ringZ = ringM + 2 * 5 * C::RP;
+    T* const ringP = ringZ + 2 * 9 * C::RP;
+    uint64_t* const bar = reinterpret_cast<uint64_t*>(ringP + 3 * 5 * C::RP);
+
+    const SlabGeom& g = P.g;
+    const int ntz = (g.nz + TZ - 1) / TZ;
+    const int y0 = (int(blockIdx.x) / ntz) * TY;
+    const int z0 = (int(blockIdx.x) % ntz) * TZ;
+    const int xs = xbeg + int(blockIdx.y) * chunk;
+    const int xe = min(xs + chunk, xend);
+    if (xs >= xe) return;
+    // step-1 planes: one beyond each end of the chunk unless that is beyond a wall
+    const int p_first = (xs == 0 && BC == BC_CAVITY && g.left_wall) ? 0 : xs - 1;
+    const int p_last = (xe == g.nxl && BC == BC_CAVITY && g.right_wall) ? g.nxl - 1 : xe;
+
+    const int tid = threadIdx.x;
+    // step-1 cell of this thread: box coordinates (a, b), cell (p, qy, qz)
+    const int a = tid / C::HZ, b = tid % C::HZ;
+    const bool act1 = tid < C::HY * C::HZ;
+    const int qy = y0 - 1 + a, qz = z0 - 1 + b;
+    const bool q_in = act1 && (BC == BC_PERIODIC || (qy >= 0 && qy < g.ny && qz >= 0 && qz < g.nz));
+    const bool q_tile = act1 && a >= 1 && a <= TY && b >= 1 && b <= TZ;
+    // step-2 cell of this thread
+    const int y2 = tid / TZ, z2 = tid % TZ;
+    const bool in2 = tid < TY * TZ && y0 + y2 < g.ny && z0 + z2 < g.nz;
+    // does any staged entry of this tile pull from outside [0,ny) x [0,nz)?
+    const bool edge_y = (y0 < 2) || (y0 + TY + 2 > g.ny);
+    const bool edge_z = (z0 < 2) || (z0 + TZ + 2 > g.nz);
+
+    auto ring = [&](int k, int dp) -> T* {
+        if (k < 5) return ringM + ((dp & 1) * 5 + k) * C::RP;
+        if (k < 14) return ringZ + ((dp & 1) * 9 + (k - 5)) * C::RP;
+        return ringP + (((dp + 3) % 3) * 5 + (k - 14)) * C::RP;
+    };
+    auto issue = [&](int p, int s) {  // one thread: stage plane p into buffer s
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&bar[s], C::TX_BYTES);
+        static_for<0, kQ>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            constexpr int i = slot_dir(k);
+            tma_load_3d(stage + (s * kQ + k) * C::BOXE, &tmA, &bar[s], z0 - C::ZPAD, y0 - 1 - can_cy(i),
+                        (p - can_cx(i) + 2) * kQ + k);
+        });
+    };
+
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (p_first <= p_last) issue(p_first, 0);
+        if (p_first + 1 <= p_last) issue(p_first + 1, 1);
+    }
+
+    for (int p = xs - 1; p <= xe; ++p) {
+        if (p >= p_first && p <= p_last) {
+            const int c = p - p_first, s = c & 1;
+            T* const st = stage + s * kQ * C::BOXE;
+            mbar_wait(&bar[s], uint32_t(c >> 1) & 1u);
+            const bool lwall = BC == BC_CAVITY && p == 0 && g.left_wall;
+            const bool rwall = BC == BC_CAVITY && p == g.nxl - 1 && g.right_wall;
+            if (edge_y || edge_z || lwall || rwall) {
+                // ---- fix-up of staged entries whose pull source leaves the domain ----
+                auto fix = [&](int k, int aa, int bb) {
+                    const int i = slot_dir(k);
+                    const int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
+                    const int fy = y0 - 1 + aa, fz = z0 - 1 + bb;
+                    const int sy = fy - cy, sz = fz - cz;
+                    const bool yz_out = sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz;
+                    if constexpr (BC == BC_CAVITY) {
+                        if (fy < 0 || fy >= g.ny || fz < 0 || fz >= g.nz) return;
+                        const bool out = yz_out || (cx == 1 && lwall) || (cx == -1 && rwall);
+                        if (!out) return;
+                        T v = A[cell_off(g, p, fy, fz) + (long long)slot_opp(k) * g.pq];
+                        if (cz == -1 && fz == g.nz - 1) v = v + P.lid[k];
+                        st[k * C::BOXE + aa * C::BW + bb + C::ZPAD - 1 - cz] = v;
+                    } else {
+                        if (!yz_out) return;
+                        st[k * C::BOXE + aa * C::BW + bb + C::ZPAD - 1 - cz] =
+                            A[(long long)(p - cx + 2) * g.px + (long long)k * g.pq +
+                              (long long)wrapi(sy, g.ny) * g.nzp + wrapi(sz, g.nz)];
+                    }
+                };
+                // rows / columns whose sources can leave the domain
+                const int rlo = min(max(2 - y0, 0), C::HY), rhi = min(max(g.ny - y0, rlo), C::HY);
+                const int clo = min(max(2 - z0, 0), C::HZ), chi = min(max(g.nz - z0, clo), C::HZ);
+                const int nbr = rlo + (C::HY - rhi), nbc = clo + (C::HZ - chi);
+                const int n_rows = kQ * nbr * C::HZ;
+                for (int idx = tid; idx < n_rows; idx += C::NT) {
+                    const int k = idx / (nbr * C::HZ), r = (idx / C::HZ) % nbr, bb = idx % C::HZ;
+                    fix(k, r < rlo ? r : rhi + (r - rlo), bb);
+                }
+                const int ngr = C::HY - nbr;  // rows not covered above
+                const int n_cols = kQ * ngr * nbc;
+                for (int idx = tid; idx < n_cols; idx += C::NT) {
+                    const int k = idx / (ngr * nbc), r = (idx / nbc) % ngr, cc = idx % nbc;
+                    fix(k, rlo + r, cc < clo ? cc : chi + (cc - clo));
+                }
+                if (lwall || rwall) {  // the directions pulling through an x wall, interior entries
+                    const int ngc = C::HZ - nbc;
+                    const int ngroups = (lwall ? 1 : 0) + (rwall ? 1 : 0);
+                    const int n_x = ngroups * 5 * ngr * ngc;
+                    for (int idx = tid; idx < n_x; idx += C::NT) {
+                        const int j = idx / (ngr * ngc);  // 0..4 first group, 5..9 second
+                        const int k = (lwall && j < 5) ? kSlotP0 + j : (j % 5);
+                        const int r = (idx / ngc) % ngr, cc = idx % ngc;
+                        fix(k, rlo + r, clo + cc);
+                    }
+                }
+                __syncthreads();
+            }
+            T f[kQ];
+            if (act1) {
+                static_for<0, kQ>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    f[slot_dir(k)] = st[k * C::BOXE + a * C::BW + b + C::ZPAD - 1 - can_cz(slot_dir(k))];
+                });
+            }
+            __syncthreads();  // buffer s consumed; step 2 of the previous plane finished
+            if (tid == 0 && p + 2 <= p_last) issue(p + 2, s);
+            if (q_in) {
+                bgk_collide<T>(f, P.omega);
+                // ---- step 1 pushes: direction i streams to (p + cx, a - 1 + cy, b - 1 + cz) ----
+                static_for<0, kQ>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    constexpr int i = slot_dir(k);
+                    const int da = a - 1 + can_cy(i), db = b - 1 + can_cz(i);
+                    if (da >= 0 && da < TY && db >= 0 && db < TZ) ring(k, p + can_cx(i))[da * TZ + db] = f[i];
+                });
+                if constexpr (BC == BC_CAVITY) {
+                    // ---- wall links of a tile cell: bounce-back (+ lid) into its own slot ----
+                    if (q_tile) {
+                        const int own = (a - 1) * TZ + (b - 1);
+                        const bool lw = p == 0 && g.left_wall, rw = p == g.nxl - 1 && g.right_wall;
+                        static_for<0, kQ>([&](auto kc) {
+                            constexpr int k = decltype(kc)::value;
+                            constexpr int i = slot_dir(k);
+                            constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
+                            const int sy = qy - cy, sz = qz - cz;
+                            bool out = sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz;
+                            if constexpr (cx == 1) out = out || lw;
+                            if constexpr (cx == -1) out = out || rw;
+                            if (out) {
+                                T v = f[can_opp(i)];
+                                if constexpr (cz == -1) {
+                                    if (qz == g.nz - 1) v = v + P.lid[k];
+                                }
+                                ring(k, p)[own] = v;
+                            }
+                        });
+                    }
+                }
+            }
+        } else {
+            __syncthreads();
+        }
+        __syncthreads();  // ring of destination plane p-1 complete
+        const int d = p - 1;
+        if (d >= xs && in2) {
+            T f[kQ];
+            const int t = y2 * TZ + z2;
+            static_for<0, kQ>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                f[slot_dir(k)] = ring(k, d)[t];
+            });
+            bgk_collide<T>(f, P.omega);
+            const long long off = cell_off(g, d, y0 + y2, z0 + z2);
+            static_for<0, kQ>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                __stcs(B + off + (long long)k * g.pq, f[slot_dir(k)]);
+            });
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host --
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+        else
+            cudaGetLastError();
+    });
+    return fn;
 }
 
 template <typename T>
-cudaError_t launch_k2(const T*, T*, const StepParams<T>&, int, int, cudaStream_t) {
-    return cudaErrorNotSupported;
+struct Tile;
+template <>
+struct Tile<double> {
+    static constexpr int TY = 8, TZ = 32;
+};
+template <>
+struct Tile<float> {
+    static constexpr int TY = 16, TZ = 32;
+};
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <typename T, int BC, int TY, int TZ>
+cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
+    using C = K2Cfg<T, TY, TZ>;
+    auto kern = k2_sweep<T, BC, TY, TZ>;
+    static int occ = -1;
+    if (occ < 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, C::SMEM);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) return cudaErrorInvalidConfiguration;
+    }
+    EncodeFn enc = get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    const SlabGeom& g = P.g;
+    CUtensorMap map;
+    const cuuint64_t dims[3] = {cuuint64_t(g.nz), cuuint64_t(g.ny), cuuint64_t(g.nxl + 4) * kQ};
+    const cuuint64_t strides[2] = {cuuint64_t(g.nzp) * sizeof(T), cuuint64_t(g.pq) * sizeof(T)};
+    const cuuint32_t box[3] = {cuuint32_t(C::BW), cuuint32_t(C::HY), 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    CUresult r = enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                     const_cast<T*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    // x chunks: fill the machine in whole waves; each chunk re-computes 2 halo planes of step 1
+    const long long ntiles = (long long)((g.ny + TY - 1) / TY) * ((g.nz + TZ - 1) / TZ);
+    const long long slots = (long long)num_sms() * occ;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int nch = 1; nch <= min(nxs, 64); ++nch) {
+        const int chunk = (nxs + nch - 1) / nch;
+        const long long items = ntiles * ((nxs + chunk - 1) / chunk);
+        const double waves = double((items + slots - 1) / slots);
+        const double cost = waves * (chunk + 2.5);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = nch;
+        }
+    }
+    const int chunk = (nxs + best - 1) / best;
+    const dim3 grid(unsigned(ntiles), unsigned((nxs + chunk - 1) / chunk));
+    kern<<<grid, C::NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+template <typename T>
+bool k2_supported(const SlabGeom& g) {
+    if (!get_encode()) return false;
+    // TMA: row pitch a multiple of 16 B (nzp is padded to 32 B); the combined
+    // (x, slot) dimension and the boxes fit the descriptor limits.
+    return (g.nzp * sizeof(T)) % 16 == 0 && (long long)(g.nxl + 4) * kQ < (1LL << 31) && g.nxl >= 1;
+}
+
+template <typename T>
+cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
+    if (nxs <= 0) return cudaSuccess;
+    constexpr int TY = Tile<T>::TY, TZ = Tile<T>::TZ;
+    if (P.g.bc == BC_PERIODIC) return launch_k2_impl<T, BC_PERIODIC, TY, TZ>(A, B, P, xbeg, nxs, s);
+    return launch_k2_impl<T, BC_CAVITY, TY, TZ>(A, B, P, xbeg, nxs, s);
 }
 
 template bool k2_supported<double>(const SlabGeom&);

@@ -24,7 +24,16 @@ LID = (0.05, 0.0, 0.0)
 
 
 def relerr(a, b):
+    """max |a - b| / |b| over every population (BASELINE.json:5)."""
     return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+def relerr_floor(a, b):
+    """Off-equilibrium random states (not BASELINE workloads): the rounding
+    error of a BGK update is absolute, of order eps * rho, whatever f_i is,
+    so the denominator is floored at the smallest lattice weight 1/36
+    (R-11)."""
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0 / 36.0)))
 
 
 def oracle_from_fields(cfg, n):
@@ -61,12 +70,12 @@ def test_random_populations_ragged(dims, bc, dtype):
     tau = 0.55
     with lbm.Lattice(*dims, tau, LID, dtype, bc=bc) as lat:
         lat.set_populations(f0)
-        assert relerr(lat.populations(), f0) <= TOL[dtype]
+        assert relerr_floor(lat.populations(), f0) <= TOL[dtype]
         ref = f0
         for n in (1, 2, 3):
             lat.step(n)
             ref = oracle.run(ref, bc, tau, LID, n)
-            assert relerr(lat.populations(), ref) <= TOL[dtype] * (10 if dtype == "f32" else 1)
+            assert relerr_floor(lat.populations(), ref) <= TOL[dtype]
 
 
 def test_config2_full_with_mass():
@@ -116,7 +125,7 @@ def test_local_slabs_bitwise(bc, slabs):
         many = lat.populations()
         r, u = lat.macroscopic()
     assert np.array_equal(one, many)
-    assert relerr(many, oracle.run(f0, bc, 0.6, LID, 5)) <= 1e-12
+    assert relerr_floor(many, oracle.run(f0, bc, 0.6, LID, 5)) <= 1e-12
 
 
 def test_init_equilibrium_local_slabs():
@@ -148,7 +157,7 @@ def test_zero_steps_roundtrip_and_errors():
             lat.step(1)
         lat.set_populations(f0)
         lat.step(0)
-        assert relerr(lat.populations(), f0) <= 1e-15
+        assert relerr_floor(lat.populations(), f0) <= 1e-15
         with pytest.raises(lbm.LbmError):
             lat.step(-1)
         bad = f0.copy()
@@ -175,3 +184,46 @@ def test_rest_state_and_lid_closed_form():
         lat.step(100)
         g = lat.populations()
     assert np.max(np.abs(g - w[:, None, None, None])) <= 1e-15
+
+
+K2_DIMS = [(1, 8, 32), (2, 5, 7), (3, 9, 33), (7, 8, 32), (16, 16, 64), (5, 17, 31), (33, 10, 70), (12, 24, 96),
+           (64, 11, 40)]
+
+
+@pytest.mark.parametrize("dims", K2_DIMS)
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_k2_equals_k1_bitwise(dims, bc, dtype):
+    """The two-step TMA sweep (K2) reproduces two one-step sweeps (K1) bit
+    for bit: ragged tiles, tiles touching every wall, x-chunk seams, thin
+    slabs, both BCs, both dtypes; and both match the oracle."""
+    if bc == lbm.LBM_BC_PERIODIC and dims[0] < 2:
+        pytest.skip("periodic needs >= 2 planes")
+    f0 = li.random_populations(31, *dims)
+    res = {}
+    for kernel in (lbm.LBM_KERNEL_K1, lbm.LBM_KERNEL_K2):
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=bc, kernel=kernel) as lat:
+            lat.set_populations(f0)
+            lat.step(4)
+            res[kernel] = lat.populations()
+            st = lbm.lbm_get_stats(lat.ctx)
+            if kernel == lbm.LBM_KERNEL_K2:
+                assert st.k2_launches == 2 and st.k1_launches == 0
+    assert np.array_equal(res[lbm.LBM_KERNEL_K1], res[lbm.LBM_KERNEL_K2])
+    assert relerr_floor(res[lbm.LBM_KERNEL_K2], oracle.run(f0, bc, 0.6, LID, 4)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
+def test_k2_local_slabs_bitwise(bc):
+    dims = (32, 20, 40)
+    f0 = li.random_populations(32, *dims)
+    outs = []
+    for kernel, slabs in [(lbm.LBM_KERNEL_K1, 1), (lbm.LBM_KERNEL_K2, 1), (lbm.LBM_KERNEL_K2, 2),
+                          (lbm.LBM_KERNEL_K2, 8)]:
+        comm = lbm.LBM_COMM_LOCAL if slabs > 1 else lbm.LBM_COMM_NONE
+        with lbm.Lattice(*dims, 0.55, LID, "f64", bc=bc, kernel=kernel, comm=comm, local_slabs=slabs) as lat:
+            lat.set_populations(f0)
+            lat.step(6)
+            outs.append(lat.populations())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
