@@ -95,6 +95,12 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// slot-order direction tables for the (runtime-indexed) fix-up path
+__constant__ signed char c_slot_cx[kQ] = {-1, -1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1};
+__constant__ signed char c_slot_cy[kQ] = {0, -1, 1, 0, 0, 0, -1, 0, -1, -1, 1, 0, 1, 1, 0, 1, -1, 0, 0};
+__constant__ signed char c_slot_cz[kQ] = {0, 0, 0, -1, 1, 0, 0, -1, -1, 1, 0, 1, 1, -1, 0, 0, 0, 1, -1};
+__constant__ signed char c_slot_opp[kQ] = {14, 15, 16, 17, 18, 5, 10, 11, 12, 13, 6, 7, 8, 9, 0, 1, 2, 3, 4};
+
 __device__ __forceinline__ int wrapi(int v, int n) {
     v %= n;
     return v < 0 ? v + n : v;
@@ -139,11 +145,6 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, 1)
     const bool edge_y = (y0 < 2) || (y0 + TY + 2 > g.ny);
     const bool edge_z = (z0 < 2) || (z0 + TZ + 2 > g.nz);
 
-    auto ring = [&](int k, int dp) -> T* {
-        if (k < 5) return ringM + ((dp & 1) * 5 + k) * C::RP;
-        if (k < 14) return ringZ + ((dp & 1) * 9 + (k - 5)) * C::RP;
-        return ringP + (((dp + 3) % 3) * 5 + (k - 14)) * C::RP;
-    };
     auto issue = [&](int p, int s) {  // one thread: stage plane p into buffer s
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_expect_tx(&bar[s], C::TX_BYTES);
@@ -167,7 +168,22 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, 1)
         if (p_first + 1 <= p_last) issue(p_first + 1, 1);
     }
 
+    // per-thread constants of the hot loop
+    const int soff = a * C::BW + b + C::ZPAD - 1;  // staged entry of (a, b) for c_z = 0
+    const int toff = (a - 1) * TZ + (b - 1);        // ring entry of this cell (tile coords)
+    // is the push destination (a - 1 + c_y, b - 1 + c_z) inside the tile, per c_y / c_z
+    const bool rowok[3] = {a >= 2 && a <= TY + 1, a >= 1 && a <= TY, a <= TY - 1};
+    const bool colok[3] = {b >= 2 && b <= TZ + 1, b >= 1 && b <= TZ, b <= TZ - 1};
+    const bool edge_tile = BC == BC_CAVITY && (edge_y || edge_z);
+
     for (int p = xs - 1; p <= xe; ++p) {
+        // ring bases: regular pushes of plane p go to destination planes p-1 (M),
+        // p (Z), p+1 (P); step 2 reads destination p-1; wall links fill p.
+        T* const rM = ringM + ((p - 1) & 1) * 5 * C::RP;  // M: written and read for dest p-1
+        T* const wZ = ringZ + (p & 1) * 9 * C::RP;
+        T* const rZ = ringZ + ((p - 1) & 1) * 9 * C::RP;
+        T* const wP = ringP + ((p + 1) % 3) * 5 * C::RP;
+        T* const rP = ringP + ((p + 2) % 3) * 5 * C::RP;
         if (p >= p_first && p <= p_last) {
             const int c = p - p_first, s = c & 1;
             T* const st = stage + s * kQ * C::BOXE;
@@ -177,8 +193,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, 1)
             if (edge_y || edge_z || lwall || rwall) {
                 // ---- fix-up of staged entries whose pull source leaves the domain ----
                 auto fix = [&](int k, int aa, int bb) {
-                    const int i = slot_dir(k);
-                    const int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
+                    const int cx = c_slot_cx[k], cy = c_slot_cy[k], cz = c_slot_cz[k];
                     const int fy = y0 - 1 + aa, fz = z0 - 1 + bb;
                     const int sy = fy - cy, sz = fz - cz;
                     const bool yz_out = sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz;
@@ -186,7 +201,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, 1)
                         if (fy < 0 || fy >= g.ny || fz < 0 || fz >= g.nz) return;
                         const bool out = yz_out || (cx == 1 && lwall) || (cx == -1 && rwall);
                         if (!out) return;
-                        T v = A[cell_off(g, p, fy, fz) + (long long)slot_opp(k) * g.pq];
+                        T v = A[cell_off(g, p, fy, fz) + (long long)c_slot_opp[k] * g.pq];
                         if (cz == -1 && fz == g.nz - 1) v = v + P.lid[k];
                         st[k * C::BOXE + aa * C::BW + bb + C::ZPAD - 1 - cz] = v;
                     } else {
@@ -226,9 +241,10 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, 1)
             }
             T f[kQ];
             if (act1) {
+                const T* const sp = st + soff;
                 static_for<0, kQ>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
-                    f[slot_dir(k)] = st[k * C::BOXE + a * C::BW + b + C::ZPAD - 1 - can_cz(slot_dir(k))];
+                    f[slot_dir(k)] = sp[k * C::BOXE - can_cz(slot_dir(k))];
                 });
             }
             __syncthreads();  // buffer s consumed; step 2 of the previous plane finished
@@ -239,28 +255,35 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, 1)
                 static_for<0, kQ>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
                     constexpr int i = slot_dir(k);
-                    const int da = a - 1 + can_cy(i), db = b - 1 + can_cz(i);
-                    if (da >= 0 && da < TY && db >= 0 && db < TZ) ring(k, p + can_cx(i))[da * TZ + db] = f[i];
+                    constexpr int cy = can_cy(i), cz = can_cz(i);
+                    constexpr int rel = cy * TZ + cz;
+                    if (rowok[cy + 1] && colok[cz + 1]) {
+                        if constexpr (k < 5) rM[k * C::RP + toff + rel] = f[i];
+                        else if constexpr (k < 14) wZ[(k - 5) * C::RP + toff + rel] = f[i];
+                        else wP[(k - 14) * C::RP + toff + rel] = f[i];
+                    }
                 });
                 if constexpr (BC == BC_CAVITY) {
                     // ---- wall links of a tile cell: bounce-back (+ lid) into its own slot ----
-                    if (q_tile) {
-                        const int own = (a - 1) * TZ + (b - 1);
-                        const bool lw = p == 0 && g.left_wall, rw = p == g.nxl - 1 && g.right_wall;
+                    if ((edge_tile || lwall || rwall) && q_tile) {
+                        T* const bM = ringM + (p & 1) * 5 * C::RP;
+                        T* const bP = ringP + (p % 3) * 5 * C::RP;
                         static_for<0, kQ>([&](auto kc) {
                             constexpr int k = decltype(kc)::value;
                             constexpr int i = slot_dir(k);
                             constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
                             const int sy = qy - cy, sz = qz - cz;
                             bool out = sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz;
-                            if constexpr (cx == 1) out = out || lw;
-                            if constexpr (cx == -1) out = out || rw;
+                            if constexpr (cx == 1) out = out || lwall;
+                            if constexpr (cx == -1) out = out || rwall;
                             if (out) {
                                 T v = f[can_opp(i)];
                                 if constexpr (cz == -1) {
                                     if (qz == g.nz - 1) v = v + P.lid[k];
                                 }
-                                ring(k, p)[own] = v;
+                                if constexpr (k < 5) bM[k * C::RP + toff] = v;
+                                else if constexpr (k < 14) wZ[(k - 5) * C::RP + toff] = v;
+                                else bP[(k - 14) * C::RP + toff] = v;
                             }
                         });
                     }
@@ -276,7 +299,9 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, 1)
             const int t = y2 * TZ + z2;
             static_for<0, kQ>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                f[slot_dir(k)] = ring(k, d)[t];
+                if constexpr (k < 5) f[slot_dir(k)] = rM[k * C::RP + t];
+                else if constexpr (k < 14) f[slot_dir(k)] = rZ[(k - 5) * C::RP + t];
+                else f[slot_dir(k)] = rP[(k - 14) * C::RP + t];
             });
             bgk_collide<T>(f, P.omega);
             const long long off = cell_off(g, d, y0 + y2, z0 + z2);
