@@ -30,6 +30,8 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "kernels.h"
@@ -56,6 +58,13 @@ struct K2Cfg {
     static constexpr int RING = (2 * 5 + 2 * 9 + 3 * 5) * RP;  // 43 direction-planes
     static constexpr size_t SMEM = size_t(2 * kQ * BOXE + RING) * sizeof(T) + 2 * sizeof(uint64_t);
     static constexpr uint32_t TX_BYTES = uint32_t(kQ * BOX * sizeof(T));
+    // CTAs per SM: what shared memory (228 KB per SM, 1 KB reserved per CTA)
+    // and registers (about 168 per thread in fp64, 96 in fp32) allow
+    static constexpr bool FITS = SMEM <= 227 * 1024;
+    static constexpr int BY_SMEM = int((228 * 1024) / (SMEM + 1024));
+    static constexpr int BY_REGS = 65536 / (NT * (sizeof(T) == 8 ? 168 : 96));
+    static constexpr int MINB_RAW = BY_SMEM < BY_REGS ? BY_SMEM : BY_REGS;
+    static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 3 ? 3 : MINB_RAW);
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -109,7 +118,7 @@ __device__ __forceinline__ int wrapi(int v, int n) {
 }  // namespace
 
 template <typename T, int BC, int TY, int TZ>
-__global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, 1)
+__global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     k2_sweep(const __grid_constant__ CUtensorMap tmA, const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
              int xbeg, int xend, int chunk) {
     using C = K2Cfg<T, TY, TZ>;
@@ -335,16 +344,22 @@ EncodeFn get_encode() {
     return fn;
 }
 
-template <typename T>
-struct Tile;
-template <>
-struct Tile<double> {
-    static constexpr int TY = 8, TZ = 32;
-};
-template <>
-struct Tile<float> {
-    static constexpr int TY = 16, TZ = 32;
-};
+// Tile shape (TY x TZ output cells per CTA).  LBM_K2_TILE=<TY>x<TZ> selects
+// one of the compiled shapes (tuning runs); the default is the measured best.
+int tile_choice(int esize) {
+    static int choice[2] = {-1, -1};
+    int& c = choice[esize == 8 ? 0 : 1];
+    if (c < 0) {
+        c = 0;
+        if (const char* e = getenv("LBM_K2_TILE")) {
+            if (!strcmp(e, "8x32")) c = 1;
+            else if (!strcmp(e, "8x16")) c = 2;
+            else if (!strcmp(e, "16x16")) c = 3;
+            else if (!strcmp(e, "16x32")) c = 4;
+        }
+    }
+    return c;
+}
 
 int num_sms() {
     static int n = 0;
@@ -415,9 +430,27 @@ bool k2_supported(const SlabGeom& g) {
 template <typename T>
 cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
     if (nxs <= 0) return cudaSuccess;
-    constexpr int TY = Tile<T>::TY, TZ = Tile<T>::TZ;
-    if (P.g.bc == BC_PERIODIC) return launch_k2_impl<T, BC_PERIODIC, TY, TZ>(A, B, P, xbeg, nxs, s);
-    return launch_k2_impl<T, BC_CAVITY, TY, TZ>(A, B, P, xbeg, nxs, s);
+    const bool per = P.g.bc == BC_PERIODIC;
+#define LBM_K2_TILE_CASE(TY, TZ)                                                     \
+    if constexpr (K2Cfg<T, TY, TZ>::FITS) {                                          \
+        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ>(A, B, P, xbeg, nxs, s)   \
+                   : launch_k2_impl<T, BC_CAVITY, TY, TZ>(A, B, P, xbeg, nxs, s);    \
+    } else {                                                                         \
+        return cudaErrorInvalidConfiguration;                                        \
+    }
+    switch (tile_choice(sizeof(T))) {
+        case 1: LBM_K2_TILE_CASE(8, 32);
+        case 2: LBM_K2_TILE_CASE(8, 16);
+        case 3: LBM_K2_TILE_CASE(16, 16);
+        case 4: LBM_K2_TILE_CASE(16, 32);
+        default:
+            if constexpr (sizeof(T) == 8) {
+                LBM_K2_TILE_CASE(8, 32);
+            } else {
+                LBM_K2_TILE_CASE(16, 32);
+            }
+    }
+#undef LBM_K2_TILE_CASE
 }
 
 template bool k2_supported<double>(const SlabGeom&);
