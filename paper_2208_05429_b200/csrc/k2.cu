@@ -55,7 +55,9 @@ struct K2Cfg {
     static constexpr int BOXE = round_up_c(BOX * int(sizeof(T)), 128) / int(sizeof(T));  // 128 B aligned
     static constexpr int NT = round_up_c(HY * HZ, 32);         // threads: one per T+1 cell
     static constexpr int RP = TY * TZ;                         // ring plane (one direction)
-    static constexpr int RING = (2 * 5 + 2 * 9 + 3 * 5) * RP;  // 43 direction-planes
+    // ring depth per group (destination planes live at once, see the loop)
+    static constexpr int NM = 2, NZ = 3, NP = 4;
+    static constexpr int RING = (NM * 5 + NZ * 9 + NP * 5) * RP;  // 57 direction-planes
     static constexpr size_t SMEM = size_t(2 * kQ * BOXE + RING) * sizeof(T) + 2 * sizeof(uint64_t);
     static constexpr uint32_t TX_BYTES = uint32_t(kQ * BOX * sizeof(T));
     // CTAs per SM: what shared memory (228 KB per SM, 1 KB reserved per CTA)
@@ -125,9 +127,9 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* const stage = reinterpret_cast<T*>(smem_raw);
     T* const ringM = stage + 2 * kQ * C::BOXE;
-    T* const ringZ = ringM + 2 * 5 * C::RP;
-    T* const ringP = ringZ + 2 * 9 * C::RP;
-    uint64_t* const bar = reinterpret_cast<uint64_t*>(ringP + 3 * 5 * C::RP);
+    T* const ringZ = ringM + C::NM * 5 * C::RP;
+    T* const ringP = ringZ + C::NZ * 9 * C::RP;
+    uint64_t* const bar = reinterpret_cast<uint64_t*>(ringP + C::NP * 5 * C::RP);
 
     const SlabGeom& g = P.g;
     const int ntz = (g.nz + TZ - 1) / TZ;
@@ -185,20 +187,25 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool colok[3] = {b >= 2 && b <= TZ + 1, b >= 1 && b <= TZ, b <= TZ - 1};
     const bool edge_tile = BC == BC_CAVITY && (edge_y || edge_z);
 
-    for (int p = xs - 1; p <= xe; ++p) {
-        // ring bases: regular pushes of plane p go to destination planes p-1 (M),
-        // p (Z), p+1 (P); step 2 reads destination p-1; wall links fill p.
-        T* const rM = ringM + ((p - 1) & 1) * 5 * C::RP;  // M: written and read for dest p-1
-        T* const wZ = ringZ + (p & 1) * 9 * C::RP;
-        T* const rZ = ringZ + ((p - 1) & 1) * 9 * C::RP;
-        T* const wP = ringP + ((p + 1) % 3) * 5 * C::RP;
-        T* const rP = ringP + ((p + 2) % 3) * 5 * C::RP;
-        if (p >= p_first && p <= p_last) {
-            const int c = p - p_first, s = c & 1;
-            T* const st = stage + s * kQ * C::BOXE;
+    // Software pipeline, ONE block barrier per plane.  Iteration p runs, in
+    // the same phase, step 2 of destination plane p-2 (complete since the
+    // previous barrier) and step 1 of plane p, whose pushes go to destination
+    // planes p-1 (c_x = -1), p (c_x = 0, and wall links) and p+1 (c_x = +1).
+    // Ring depths keep reads and writes of one phase apart: M 2 (dest p-2
+    // read / p-1 written), Z 3 (p-2 read, p-1 live, p written), P 4 (p-2
+    // read, p-1 and p live, p+1 written).  Bounce-back links of c_x = -1
+    // directions (dest p) are held in registers and written next iteration
+    // with the regular pushes of dest p, so M needs only two planes.
+    T heldP[5];  // f*_opp of the c_x = -1 wall links of the previous plane (+ lid)
+    unsigned held_mask = 0;
+    for (int p = xs - 1; p <= xe + 1; ++p) {
+        const bool has1 = p >= p_first && p <= p_last;
+        const int c = p - p_first, s = c & 1;
+        T* const st = stage + s * kQ * C::BOXE;
+        const bool lwall = BC == BC_CAVITY && p == 0 && g.left_wall;
+        const bool rwall = BC == BC_CAVITY && p == g.nxl - 1 && g.right_wall;
+        if (has1) {
             mbar_wait(&bar[s], uint32_t(c >> 1) & 1u);
-            const bool lwall = BC == BC_CAVITY && p == 0 && g.left_wall;
-            const bool rwall = BC == BC_CAVITY && p == g.nxl - 1 && g.right_wall;
             if (edge_y || edge_z || lwall || rwall) {
                 // ---- fix-up of staged entries whose pull source leaves the domain ----
                 auto fix = [&](int k, int aa, int bb) {
@@ -248,6 +255,43 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 }
                 __syncthreads();
             }
+        }
+        // ---------------- step 2: destination plane d = p - 2 ----------------
+        const int d = p - 2;
+        if (d >= xs && in2) {
+            const T* const qM = ringM + (d & 1) * 5 * C::RP;
+            const T* const qZ = ringZ + (d % 3) * 9 * C::RP;
+            const T* const qP = ringP + (d & 3) * 5 * C::RP;
+            T f[kQ];
+            const int t = y2 * TZ + z2;
+            static_for<0, kQ>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                if constexpr (k < 5) f[slot_dir(k)] = qM[k * C::RP + t];
+                else if constexpr (k < 14) f[slot_dir(k)] = qZ[(k - 5) * C::RP + t];
+                else f[slot_dir(k)] = qP[(k - 14) * C::RP + t];
+            });
+            bgk_collide<T>(f, P.omega);
+            const long long off = cell_off(g, d, y0 + y2, z0 + z2);
+            static_for<0, kQ>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                __stcs(B + off + (long long)k * g.pq, f[slot_dir(k)]);
+            });
+        }
+        // ---------------- step 1: plane p ----------------
+        T* const wM = ringM + ((p + 1) & 1) * 5 * C::RP;  // dest p-1 (p + 1 has the parity of p - 1)
+        T* const wZ = ringZ + ((p + 3) % 3) * 9 * C::RP;  // dest p
+        T* const wP = ringP + ((p + 1) & 3) * 5 * C::RP;  // dest p+1
+        if constexpr (BC == BC_CAVITY) {
+            // wall links of c_x = -1 directions held from plane p-1 -> dest p-1
+            if (held_mask) {
+                static_for<0, 5>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    if (held_mask & (1u << k)) wM[k * C::RP + toff] = heldP[k];
+                });
+                held_mask = 0;
+            }
+        }
+        if (has1) {
             T f[kQ];
             if (act1) {
                 const T* const sp = st + soff;
@@ -256,18 +300,16 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                     f[slot_dir(k)] = sp[k * C::BOXE - can_cz(slot_dir(k))];
                 });
             }
-            __syncthreads();  // buffer s consumed; step 2 of the previous plane finished
-            if (tid == 0 && p + 2 <= p_last) issue(p + 2, s);
             if (q_in) {
                 bgk_collide<T>(f, P.omega);
-                // ---- step 1 pushes: direction i streams to (p + cx, a - 1 + cy, b - 1 + cz) ----
+                // ---- pushes: direction i streams to (p + cx, a - 1 + cy, b - 1 + cz) ----
                 static_for<0, kQ>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
                     constexpr int i = slot_dir(k);
                     constexpr int cy = can_cy(i), cz = can_cz(i);
                     constexpr int rel = cy * TZ + cz;
                     if (rowok[cy + 1] && colok[cz + 1]) {
-                        if constexpr (k < 5) rM[k * C::RP + toff + rel] = f[i];
+                        if constexpr (k < 5) wM[k * C::RP + toff + rel] = f[i];
                         else if constexpr (k < 14) wZ[(k - 5) * C::RP + toff + rel] = f[i];
                         else wP[(k - 14) * C::RP + toff + rel] = f[i];
                     }
@@ -275,8 +317,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 if constexpr (BC == BC_CAVITY) {
                     // ---- wall links of a tile cell: bounce-back (+ lid) into its own slot ----
                     if ((edge_tile || lwall || rwall) && q_tile) {
-                        T* const bM = ringM + (p & 1) * 5 * C::RP;
-                        T* const bP = ringP + (p % 3) * 5 * C::RP;
+                        T* const bP = ringP + (p & 3) * 5 * C::RP;  // dest p
                         static_for<0, kQ>([&](auto kc) {
                             constexpr int k = decltype(kc)::value;
                             constexpr int i = slot_dir(k);
@@ -290,35 +331,22 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                                 if constexpr (cz == -1) {
                                     if (qz == g.nz - 1) v = v + P.lid[k];
                                 }
-                                if constexpr (k < 5) bM[k * C::RP + toff] = v;
-                                else if constexpr (k < 14) wZ[(k - 5) * C::RP + toff] = v;
-                                else bP[(k - 14) * C::RP + toff] = v;
+                                if constexpr (k < 5) {
+                                    heldP[k] = v;
+                                    held_mask |= 1u << k;
+                                } else if constexpr (k < 14) {
+                                    wZ[(k - 5) * C::RP + toff] = v;
+                                } else {
+                                    bP[(k - 14) * C::RP + toff] = v;
+                                }
                             }
                         });
                     }
                 }
             }
-        } else {
-            __syncthreads();
         }
-        __syncthreads();  // ring of destination plane p-1 complete
-        const int d = p - 1;
-        if (d >= xs && in2) {
-            T f[kQ];
-            const int t = y2 * TZ + z2;
-            static_for<0, kQ>([&](auto kc) {
-                constexpr int k = decltype(kc)::value;
-                if constexpr (k < 5) f[slot_dir(k)] = rM[k * C::RP + t];
-                else if constexpr (k < 14) f[slot_dir(k)] = rZ[(k - 5) * C::RP + t];
-                else f[slot_dir(k)] = rP[(k - 14) * C::RP + t];
-            });
-            bgk_collide<T>(f, P.omega);
-            const long long off = cell_off(g, d, y0 + y2, z0 + z2);
-            static_for<0, kQ>([&](auto kc) {
-                constexpr int k = decltype(kc)::value;
-                __stcs(B + off + (long long)k * g.pq, f[slot_dir(k)]);
-            });
-        }
+        __syncthreads();  // stage of plane p consumed; ring of destination p-1 complete
+        if (tid == 0 && has1 && p + 2 <= p_last) issue(p + 2, s);
     }
 }
 
