@@ -74,9 +74,15 @@ typedef enum {
 
 /* Sweep kernel selection.  K1: one fused collide+stream step per HBM pass
  * (Alg. 1's loop fusion).  K2: two steps per HBM pass, temporally blocked
- * in shared memory (Alg. 2's two-step merge); an odd remainder uses K1.
- * AUTO picks K2 where available.  Results are bitwise identical. */
-typedef enum { LBM_KERNEL_AUTO = 0, LBM_KERNEL_K1 = 1, LBM_KERNEL_K2 = 2 } lbm_kernel;
+ * on chip (Alg. 2's two-step merge): TMA-staged shared-memory tiles where the
+ * TMA descriptor can describe the slab (z pitch a multiple of 16 bytes,
+ * (nx_local+4)*19 < 2^31), otherwise the cp.async-staged variant K2_REG; an
+ * odd remainder uses K1.  K2_REG: force the cp.async-staged, warp-specialised
+ * variant (kept for A/B measurement; needs 19*ny*nz_pitch*sizeof(T) < 2^30).
+ * AUTO = K2, falling back to K1 pairs where no two-step variant fits; an
+ * explicit K2/K2_REG on such a slab gives EINVAL from lbm_step.  Results are
+ * bitwise identical whichever kernel runs. */
+typedef enum { LBM_KERNEL_AUTO = 0, LBM_KERNEL_K1 = 1, LBM_KERNEL_K2 = 2, LBM_KERNEL_K2_REG = 3 } lbm_kernel;
 
 /* Halo transport between X-slabs (PAPER.md:336 X-only partition).
  *  NONE   world == 1 and local_slabs == 1 (periodic x wraps onto itself)

@@ -272,10 +272,18 @@ lbm_status prof_end(lbm_ctx* c, size_t slot, long long updates) {
 // --------------------------------------------------------------- engine --
 template <typename T>
 lbm_status run_steps(lbm_ctx* c, long n) {
+    // AUTO and K2: the TMA-staged two-step sweep (k2.cu) where the TMA
+    // descriptor can describe the slab, else the cp.async-staged one (K2R,
+    // k2r.cu); K2_REG forces K2R.  AUTO falls back to K1 pairs when neither
+    // fits; an explicit two-step request then fails.
+    const bool reg_only = c->opts.kernel == LBM_KERNEL_K2_REG;
+    bool tma = !reg_only && c->opts.kernel != LBM_KERNEL_K1;
+    for (const Slab& s : c->slabs) tma = tma && k2_supported<T>(s.g);
     bool use_k2 = c->opts.kernel != LBM_KERNEL_K1;
-    for (const Slab& s : c->slabs) use_k2 = use_k2 && k2_supported<T>(s.g);
-    if (c->opts.kernel == LBM_KERNEL_K2 && !use_k2 && n >= 2)
-        return fail(c, LBM_EINVAL, "K2 requested but not supported for this geometry");
+    if (!tma)
+        for (const Slab& s : c->slabs) use_k2 = use_k2 && k2r_supported<T>(s.g);
+    if (c->opts.kernel >= LBM_KERNEL_K2 && !use_k2 && n >= 2)
+        return fail(c, LBM_EINVAL, "two-step kernel requested but not supported for this geometry");
     while (n > 0) {
         const int nsteps = (use_k2 && n >= 2) ? 2 : 1;
         if (!c->ghosts_valid && has_neighbours(c)) {
@@ -289,8 +297,9 @@ lbm_status run_steps(lbm_ctx* c, long n) {
             size_t slot = 0;
             lbm_status st = prof_begin(c, slot);
             if (st != LBM_OK) return st;
-            cudaError_t e = nsteps == 2 ? launch_k2<T>(A, B, P, 0, s.g.nxl, c->stream)
-                                        : launch_k1<T>(A, B, P, 0, s.g.nxl, c->stream);
+            cudaError_t e = nsteps == 1 ? launch_k1<T>(A, B, P, 0, s.g.nxl, c->stream)
+                            : tma       ? launch_k2<T>(A, B, P, 0, s.g.nxl, c->stream)
+                                        : launch_k2r<T>(A, B, P, 0, s.g.nxl, c->stream);
             if (e != cudaSuccess)
                 return fail(c, LBM_ECUDA, "sweep launch failed: %s", cudaGetErrorString(e));
             c->launches++;
@@ -545,7 +554,7 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         return fail(c, LBM_EINVAL, "comm NCCL needs local_slabs == 1 and an nccl_id");
     if (o.comm == LBM_COMM_LOCAL && o.world != 1) return fail(c, LBM_EINVAL, "comm LOCAL needs world == 1");
     if (o.comm < LBM_COMM_NONE || o.comm > LBM_COMM_LOCAL) return fail(c, LBM_EINVAL, "bad comm %d", o.comm);
-    if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K2) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K2_REG) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
     const int nslab_total = o.world * o.local_slabs;
     if (nx % nslab_total) return fail(c, LBM_EINVAL, "nx %d not divisible by %d slabs", nx, nslab_total);
     const int nxl = nx / nslab_total;

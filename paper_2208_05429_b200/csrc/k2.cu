@@ -119,7 +119,7 @@ __device__ __forceinline__ int wrapi(int v, int n) {
 
 }  // namespace
 
-template <typename T, int BC, int TY, int TZ>
+template <typename T, int BC, int TY, int TZ, bool EARLY>
 __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     k2_sweep(const __grid_constant__ CUtensorMap tmA, const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
              int xbeg, int xend, int chunk) {
@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     // step-2 cell of this thread
     const int y2 = tid / TZ, z2 = tid % TZ;
     const bool in2 = tid < TY * TZ && y0 + y2 < g.ny && z0 + z2 < g.nz;
+    const bool warp2 = (tid & ~31) < TY * TZ;  // the warp owns step-2 cells (warp-uniform)
     // does any staged entry of this tile pull from outside [0,ny) x [0,nz)?
     const bool edge_y = (y0 < 2) || (y0 + TY + 2 > g.ny);
     const bool edge_z = (z0 < 2) || (z0 + TZ + 2 > g.nz);
@@ -187,9 +188,9 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool colok[3] = {b >= 2 && b <= TZ + 1, b >= 1 && b <= TZ, b <= TZ - 1};
     const bool edge_tile = BC == BC_CAVITY && (edge_y || edge_z);
 
-    // Software pipeline, ONE block barrier per plane.  Iteration p runs, in
-    // the same phase, step 2 of destination plane p-2 (complete since the
-    // previous barrier) and step 1 of plane p, whose pushes go to destination
+    // Software pipeline, ONE block barrier per plane (after the stage read).
+    // Iteration p runs, in the same phase, step 2 of destination plane p-2
+    // (complete since this iteration's barrier) and step 1 of plane p, whose pushes go to destination
     // planes p-1 (c_x = -1), p (c_x = 0, and wall links) and p+1 (c_x = +1).
     // Ring depths keep reads and writes of one phase apart: M 2 (dest p-2
     // read / p-1 written), Z 3 (p-2 read, p-1 live, p written), P 4 (p-2
@@ -256,28 +257,59 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 __syncthreads();
             }
         }
-        // ---------------- step 2: destination plane d = p - 2 ----------------
+        // Read this thread's staged f(t) into registers, then ONE barrier:
+        // the stage buffer is free and the TMA of plane p+2 is issued before
+        // any collision of this iteration, so every load has two compute
+        // phases to land (an effective third pipeline stage without a third
+        // buffer).  The barrier also orders step 1 of plane p-1 (last
+        // iteration's pushes) before step 2 of plane p-2 below.
+        T fs[kQ];
+        auto read_stage = [&] {
+            if (has1) {
+                const T* const sp = st + (act1 ? soff : C::ZPAD);
+                static_for<0, kQ>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    fs[slot_dir(k)] = sp[k * C::BOXE - can_cz(slot_dir(k))];
+                });
+            }
+        };
+        if constexpr (EARLY) {
+            read_stage();
+            __syncthreads();
+            if (tid == 0 && has1 && p + 2 <= p_last) issue(p + 2, s);
+        }
+        // ---------------- step 2 of dest plane d = p - 2, step 1 of plane p ----------------
+        // A thread owns (up to) one cell of each; the two collisions are
+        // independent, so they run as two interleaved dependency chains
+        // (bgk_collide2: twice the ILP of back-to-back collisions).  Warps
+        // that own no step-2 cell (warp-uniform) collide their step-1 cell alone.
         const int d = p - 2;
-        if (d >= xs && in2) {
+        const bool do2 = d >= xs && warp2;
+        T f2[kQ];
+        if (do2) {
             const T* const qM = ringM + (d & 1) * 5 * C::RP;
             const T* const qZ = ringZ + (d % 3) * 9 * C::RP;
             const T* const qP = ringP + (d & 3) * 5 * C::RP;
-            T f[kQ];
-            const int t = y2 * TZ + z2;
+            const int t = in2 ? y2 * TZ + z2 : 0;
             static_for<0, kQ>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                if constexpr (k < 5) f[slot_dir(k)] = qM[k * C::RP + t];
-                else if constexpr (k < 14) f[slot_dir(k)] = qZ[(k - 5) * C::RP + t];
-                else f[slot_dir(k)] = qP[(k - 14) * C::RP + t];
+                if constexpr (k < 5) f2[slot_dir(k)] = qM[k * C::RP + t];
+                else if constexpr (k < 14) f2[slot_dir(k)] = qZ[(k - 5) * C::RP + t];
+                else f2[slot_dir(k)] = qP[(k - 14) * C::RP + t];
             });
-            bgk_collide<T>(f, P.omega);
+        }
+        if constexpr (!EARLY) read_stage();
+        if (do2 && has1) bgk_collide2<T>(f2, fs, P.omega);
+        else if (do2) bgk_collide<T>(f2, P.omega);
+        else if (has1) bgk_collide<T>(fs, P.omega);
+        if (do2 && in2) {
             const long long off = cell_off(g, d, y0 + y2, z0 + z2);
             static_for<0, kQ>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                __stcs(B + off + (long long)k * g.pq, f[slot_dir(k)]);
+                __stcs(B + off + (long long)k * g.pq, f2[slot_dir(k)]);
             });
         }
-        // ---------------- step 1: plane p ----------------
+        // ---------------- step 1: plane p (pushes) ----------------
         T* const wM = ringM + ((p + 1) & 1) * 5 * C::RP;  // dest p-1 (p + 1 has the parity of p - 1)
         T* const wZ = ringZ + ((p + 3) % 3) * 9 * C::RP;  // dest p
         T* const wP = ringP + ((p + 1) & 3) * 5 * C::RP;  // dest p+1
@@ -292,16 +324,8 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
             }
         }
         if (has1) {
-            T f[kQ];
-            if (act1) {
-                const T* const sp = st + soff;
-                static_for<0, kQ>([&](auto kc) {
-                    constexpr int k = decltype(kc)::value;
-                    f[slot_dir(k)] = sp[k * C::BOXE - can_cz(slot_dir(k))];
-                });
-            }
+            T (&f)[kQ] = fs;
             if (q_in) {
-                bgk_collide<T>(f, P.omega);
                 // ---- pushes: direction i streams to (p + cx, a - 1 + cy, b - 1 + cz) ----
                 static_for<0, kQ>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
@@ -345,8 +369,10 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 }
             }
         }
-        __syncthreads();  // stage of plane p consumed; ring of destination p-1 complete
-        if (tid == 0 && has1 && p + 2 <= p_last) issue(p + 2, s);
+        if constexpr (!EARLY) {
+            __syncthreads();  // stage of plane p consumed; ring of destination p-1 complete
+            if (tid == 0 && has1 && p + 2 <= p_last) issue(p + 2, s);
+        }
     }
 }
 
@@ -400,10 +426,10 @@ int num_sms() {
     return n;
 }
 
-template <typename T, int BC, int TY, int TZ>
+template <typename T, int BC, int TY, int TZ, bool EARLY>
 cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
     using C = K2Cfg<T, TY, TZ>;
-    auto kern = k2_sweep<T, BC, TY, TZ>;
+    auto kern = k2_sweep<T, BC, TY, TZ, EARLY>;
     static int occ = -1;
     if (occ < 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -420,17 +446,33 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     const cuuint64_t strides[2] = {cuuint64_t(g.nzp) * sizeof(T), cuuint64_t(g.pq) * sizeof(T)};
     const cuuint32_t box[3] = {cuuint32_t(C::BW), cuuint32_t(C::HY), 1u};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
+    static CUtensorMapL2promotion promo = [] {
+        // LBM_K2_L2PROMO=none|64|128|256 (tuning runs); default 256 B
+        const char* e = getenv("LBM_K2_L2PROMO");
+        if (e && !strcmp(e, "none")) return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+        if (e && !strcmp(e, "64")) return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+        if (e && !strcmp(e, "128")) return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+        return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }();
     CUresult r = enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                      const_cast<T*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     // x chunks: fill the machine in whole waves; each chunk re-computes 2 halo planes of step 1
     const long long ntiles = (long long)((g.ny + TY - 1) / TY) * ((g.nz + TZ - 1) / TZ);
     const long long slots = (long long)num_sms() * occ;
+    // x chunks of at most kMaxChunk planes: co-resident CTAs start a chunk
+    // together and stay within a few planes of each other, so the halo rows
+    // and columns one CTA stages are still in L2 when its neighbours stage
+    // them (measured on 1024x512x512 fp64: chunk 48 33.6k MLUPS, 96 30.8k,
+    // whole-slab 27k).  Among those, fill whole waves of the machine; each
+    // chunk re-computes ~2.5 planes of step 1.
+    constexpr int kMaxChunk = 64;
     int best = 1;
     double best_cost = 1e300;
-    for (int nch = 1; nch <= min(nxs, 64); ++nch) {
+    for (int nch = 1; nch <= nxs; ++nch) {
         const int chunk = (nxs + nch - 1) / nch;
+        if (chunk > kMaxChunk && nch < nxs) continue;
         const long long items = ntiles * ((nxs + chunk - 1) / chunk);
         const double waves = double((items + slots - 1) / slots);
         const double cost = waves * (chunk + 2.5);
@@ -438,8 +480,14 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
             best_cost = cost;
             best = nch;
         }
+        if (chunk <= 8) break;
     }
-    const int chunk = (nxs + best - 1) / best;
+    int chunk = (nxs + best - 1) / best;
+    static const int force_chunk = [] {
+        const char* e = getenv("LBM_K2_CHUNK");  // planes per CTA (tuning runs)
+        return e ? atoi(e) : 0;
+    }();
+    if (force_chunk > 0) chunk = min(force_chunk, nxs);
     const dim3 grid(unsigned(ntiles), unsigned((nxs + chunk - 1) / chunk));
     kern<<<grid, C::NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk);
     return cudaGetLastError();
@@ -459,10 +507,20 @@ template <typename T>
 cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
     if (nxs <= 0) return cudaSuccess;
     const bool per = P.g.bc == BC_PERIODIC;
+    // Default: read the stage into registers and issue the next TMA before
+    // the collisions (measured faster with short chunks: fp64 33.6k vs 30.2k
+    // MLUPS); LBM_K2_EARLY=0 issues after them (tuning runs).
+    static const bool early = [] {
+        const char* e = getenv("LBM_K2_EARLY");
+        return !(e && e[0] == '0');
+    }();
 #define LBM_K2_TILE_CASE(TY, TZ)                                                     \
     if constexpr (K2Cfg<T, TY, TZ>::FITS) {                                          \
-        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ>(A, B, P, xbeg, nxs, s)   \
-                   : launch_k2_impl<T, BC_CAVITY, TY, TZ>(A, B, P, xbeg, nxs, s);    \
+        if (early)                                                                   \
+            return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true>(A, B, P, xbeg, nxs, s) \
+                       : launch_k2_impl<T, BC_CAVITY, TY, TZ, true>(A, B, P, xbeg, nxs, s);  \
+        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, false>(A, B, P, xbeg, nxs, s)   \
+                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, false>(A, B, P, xbeg, nxs, s);    \
     } else {                                                                         \
         return cudaErrorInvalidConfiguration;                                        \
     }

@@ -16,6 +16,12 @@ template <typename T>
 cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s);
 template <typename T>
 bool k2_supported(const SlabGeom& g);
+// K2R: the same two-step sweep with register-staged gathers and two warp
+// groups (k2r.cu); any geometry.
+template <typename T>
+bool k2r_supported(const SlabGeom& g);
+template <typename T>
+cudaError_t launch_k2r(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s);
 
 template <typename T>
 cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, const SlabGeom& g, cudaStream_t s);

@@ -194,23 +194,57 @@ K2_DIMS = [(1, 8, 32), (2, 5, 7), (3, 9, 33), (7, 8, 32), (16, 16, 64), (5, 17, 
 @pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_k2_equals_k1_bitwise(dims, bc, dtype):
-    """The two-step TMA sweep (K2) reproduces two one-step sweeps (K1) bit
-    for bit: ragged tiles, tiles touching every wall, x-chunk seams, thin
-    slabs, both BCs, both dtypes; and both match the oracle."""
+    """The two-step sweeps -- K2 (TMA-staged) and K2_REG (cp.async-staged,
+    warp-specialised) -- reproduce two one-step sweeps (K1) bit for bit: ragged
+    tiles, tiles touching every wall, x-chunk seams, thin slabs, both BCs,
+    both dtypes; and all match the oracle."""
     if bc == lbm.LBM_BC_PERIODIC and dims[0] < 2:
         pytest.skip("periodic needs >= 2 planes")
     f0 = li.random_populations(31, *dims)
     res = {}
-    for kernel in (lbm.LBM_KERNEL_K1, lbm.LBM_KERNEL_K2):
+    for kernel in (lbm.LBM_KERNEL_K1, lbm.LBM_KERNEL_K2, lbm.LBM_KERNEL_K2_REG):
         with lbm.Lattice(*dims, 0.6, LID, dtype, bc=bc, kernel=kernel) as lat:
             lat.set_populations(f0)
             lat.step(4)
             res[kernel] = lat.populations()
             st = lbm.lbm_get_stats(lat.ctx)
-            if kernel == lbm.LBM_KERNEL_K2:
+            if kernel != lbm.LBM_KERNEL_K1:
                 assert st.k2_launches == 2 and st.k1_launches == 0
     assert np.array_equal(res[lbm.LBM_KERNEL_K1], res[lbm.LBM_KERNEL_K2])
+    assert np.array_equal(res[lbm.LBM_KERNEL_K1], res[lbm.LBM_KERNEL_K2_REG])
     assert relerr_floor(res[lbm.LBM_KERNEL_K2], oracle.run(f0, bc, 0.6, LID, 4)) <= TOL[dtype]
+
+
+K2_VARIANTS = [("LBM_K2R_CFG", v, 3) for v in ["8x32s0", "8x32s1", "8x16s0m2", "16x16s0", "4x32s0m2", "8x16s1m2"]] + \
+    [("LBM_K2_TILE", v, 2) for v in ["8x32", "8x16", "16x16"]] + [("LBM_K2_EARLY", "0", 2), ("LBM_K2_CHUNK", "3", 2)]
+
+
+@pytest.mark.parametrize("var,shape,kernel", K2_VARIANTS)
+def test_k2_variants_bitwise(var, shape, kernel, tmp_path):
+    """Every compiled two-step variant (K2 tile TY x TZ, ring slack S, CTAs
+    per SM; K2_TMA tiles and issue order -- env vars read once per process,
+    so each runs in a subprocess) equals K1 bit for bit on ragged cavity and
+    periodic boxes in both dtypes."""
+    import subprocess
+    import sys
+    import os
+    script = tmp_path / "k2r_shape.py"
+    script.write_text(
+        "import numpy as np, lbm_inputs as li, paper_2208_05429_b200 as lbm\n"
+        "for bc in (lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC):\n"
+        "  for dims in [(5, 17, 31), (9, 21, 70), (4, 8, 32)]:\n"
+        "    for dt in ('f64', 'f32'):\n"
+        "      f0 = li.random_populations(41, *dims); r = []\n"
+        f"      for k in (lbm.LBM_KERNEL_K1, {kernel}):\n"
+        "        with lbm.Lattice(*dims, 0.6, (0.05, 0, 0), dt, bc=bc, kernel=k) as lat:\n"
+        "          lat.set_populations(f0); lat.step(4); r.append(lat.populations())\n"
+        "      assert np.array_equal(r[0], r[1]), (bc, dims, dt)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root)
+    env[var] = shape
+    out = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
 
 
 @pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
@@ -219,7 +253,7 @@ def test_k2_local_slabs_bitwise(bc):
     f0 = li.random_populations(32, *dims)
     outs = []
     for kernel, slabs in [(lbm.LBM_KERNEL_K1, 1), (lbm.LBM_KERNEL_K2, 1), (lbm.LBM_KERNEL_K2, 2),
-                          (lbm.LBM_KERNEL_K2, 8)]:
+                          (lbm.LBM_KERNEL_K2, 8), (lbm.LBM_KERNEL_K2_REG, 2)]:
         comm = lbm.LBM_COMM_LOCAL if slabs > 1 else lbm.LBM_COMM_NONE
         with lbm.Lattice(*dims, 0.55, LID, "f64", bc=bc, kernel=kernel, comm=comm, local_slabs=slabs) as lat:
             lat.set_populations(f0)

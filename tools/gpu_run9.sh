@@ -1,0 +1,15 @@
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "k2_equals_k1 or variants or local_slabs or kernel_choice" > gpurun_out/t_k2.log 2>&1; tail -2 gpurun_out/t_k2.log
+grep -q " passed" gpurun_out/t_k2.log || exit 1
+SB="timeout 120 python tools/sweep_bench.py --dims 256,512,512 --steps 40 --reps 3"
+for dt in f64 f32; do
+$SB --dtype $dt --kernel k1 --tag k1
+$SB --dtype $dt --kernel k2tma --tag tma
+LBM_K2_EARLY=1 $SB --dtype $dt --kernel k2tma --tag tma-early
+LBM_K2_L2PROMO=none $SB --dtype $dt --kernel k2tma --tag tma-promo-none
+LBM_K2_L2PROMO=128 $SB --dtype $dt --kernel k2tma --tag tma-promo-128
+for c in 8x32s0 8x32s1 8x16s0m2 16x16s0 4x32s0m2 8x16s1m2; do LBM_K2R_CFG=$c $SB --dtype $dt --kernel k2 --tag k2r-$c; done
+done
+LBM_K2_TILE=16x16 $SB --dtype f64 --kernel k2tma --tag tma16x16
+LBM_K2_TILE=8x32 $SB --dtype f32 --kernel k2tma --tag tma8x32
+$SB --dtype f64 --kernel k2tma --tag tma-again

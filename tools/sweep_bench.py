@@ -1,0 +1,51 @@
+"""Sweep-kernel micro-benchmark (tuning aid, not the bench contract): times
+the library's two-step (or one-step) sweep launches with the library's own
+CUDA events on a cavity/periodic box and prints one line per run.
+
+  python tools/sweep_bench.py --dims 256,512,512 --dtype f64 --kernel k2 --steps 40 --reps 3
+Variant shapes are selected by the env vars LBM_K2R_CFG / LBM_K2_TILE."""
+import argparse
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+import paper_2208_05429_b200 as lbm  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--dims", default="256,512,512")
+ap.add_argument("--dtype", default="f64")
+ap.add_argument("--bc", default="cavity")
+ap.add_argument("--kernel", default="k2")
+ap.add_argument("--steps", type=int, default=40)
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--tag", default="")
+a = ap.parse_args()
+nx, ny, nz = (int(v) for v in a.dims.split(","))
+kern = {"auto": 0, "k1": 1, "k2": 2, "k2reg": 3}[a.kernel]
+bc = lbm.LBM_BC_CAVITY if a.bc == "cavity" else lbm.LBM_BC_PERIODIC
+es = 8 if a.dtype == "f64" else 4
+with lbm.Lattice(nx, ny, nz, 0.6, (0.05, 0, 0), a.dtype, bc=bc, kernel=kern) as lat:
+    lat.init_equilibrium(None, None)
+    lat.step(4)
+    lbm.lbm_synchronize(lat.ctx)
+    res = []
+    for _ in range(a.reps):
+        lbm.lbm_profile_enable(lat.ctx, True)
+        lbm.lbm_profile_reset(lat.ctx)
+        lat.step(a.steps)
+        lbm.lbm_synchronize(lat.ctx)
+        st = lbm.lbm_get_stats(lat.ctx)
+        lbm.lbm_profile_enable(lat.ctx, False)
+        ms = st.sweep_ms / max(1, st.sweep_launches)
+        steps_per = st.sweep_updates / max(1, st.sweep_launches) / (nx * ny * nz)
+        mlups = nx * ny * nz * steps_per / (ms * 1e-3) / 1e6
+        res.append((mlups, ms))
+    best = max(r[0] for r in res)
+    med = statistics.median(r[0] for r in res)
+    gbs = best * 1e6 * 19 * es * (2 / steps_per) / 1e9
+    print(f"{a.tag or a.kernel:24s} {a.dtype} {a.dims:14s} best {best:9.1f} MLUPS  median {med:9.1f}  "
+          f"sweep {min(r[1] for r in res):8.3f} ms  algorithmic {gbs:7.1f} GB/s", flush=True)
