@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const int y2 = tid / TZ, z2 = tid % TZ;
     const bool in2 = tid < TY * TZ && y0 + y2 < g.ny && z0 + z2 < g.nz;
     const bool warp2 = (tid & ~31) < TY * TZ;  // the warp owns step-2 cells (warp-uniform)
+    const int st_off = (y0 + y2) * g.nzp + (z0 + z2);  // in-plane offset of the step-2 cell (< 2^31)
     // does any staged entry of this tile pull from outside [0,ny) x [0,nz)?
     const bool edge_y = (y0 < 2) || (y0 + TY + 2 > g.ny);
     const bool edge_z = (z0 < 2) || (z0 + TZ + 2 > g.nz);
@@ -303,10 +304,12 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         else if (do2) bgk_collide<T>(f2, P.omega);
         else if (has1) bgk_collide<T>(fs, P.omega);
         if (do2 && in2) {
-            const long long off = cell_off(g, d, y0 + y2, z0 + z2);
+            // slot-plane bases are CTA-uniform (uniform datapath); the
+            // thread adds its 32-bit in-plane offset: one IMAD.WIDE per store
+            T* const Bd = B + (long long)(d + 2) * g.px;
             static_for<0, kQ>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                __stcs(B + off + (long long)k * g.pq, f2[slot_dir(k)]);
+                __stcs(Bd + (long long)k * g.pq + st_off, f2[slot_dir(k)]);
             });
         }
         // ---------------- step 1: plane p (pushes) ----------------
@@ -429,12 +432,13 @@ int num_sms() {
 template <typename T, int BC, int TY, int TZ, bool EARLY>
 cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
     using C = K2Cfg<T, TY, TZ>;
+    constexpr int NT = C::NT;
     auto kern = k2_sweep<T, BC, TY, TZ, EARLY>;
     static int occ = -1;
     if (occ < 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, C::SMEM);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, C::SMEM);
         if (e != cudaSuccess) return e;
         if (occ < 1) return cudaErrorInvalidConfiguration;
     }
@@ -447,12 +451,14 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     const cuuint32_t box[3] = {cuuint32_t(C::BW), cuuint32_t(C::HY), 1u};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
     static CUtensorMapL2promotion promo = [] {
-        // LBM_K2_L2PROMO=none|64|128|256 (tuning runs); default 256 B
+        // LBM_K2_L2PROMO=none|64|128|256 (tuning runs).  Default 64 B: the
+        // least DRAM over-fetch of the halo edges (256-plane fp64 sweep:
+        // 1.18x the algorithmic reads vs 1.24x none / 1.31x 256 B), same speed.
         const char* e = getenv("LBM_K2_L2PROMO");
         if (e && !strcmp(e, "none")) return CU_TENSOR_MAP_L2_PROMOTION_NONE;
-        if (e && !strcmp(e, "64")) return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+        if (e && !strcmp(e, "256")) return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
         if (e && !strcmp(e, "128")) return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-        return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+        return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     }();
     CUresult r = enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                      const_cast<T*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -489,7 +495,7 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     }();
     if (force_chunk > 0) chunk = min(force_chunk, nxs);
     const dim3 grid(unsigned(ntiles), unsigned((nxs + chunk - 1) / chunk));
-    kern<<<grid, C::NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk);
+    kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk);
     return cudaGetLastError();
 }
 
@@ -509,20 +515,22 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
     const bool per = P.g.bc == BC_PERIODIC;
     // Default: read the stage into registers and issue the next TMA before
     // the collisions (measured faster with short chunks: fp64 33.6k vs 30.2k
-    // MLUPS); LBM_K2_EARLY=0 issues after them (tuning runs).
+    // MLUPS); LBM_K2_EARLY=0 issues after them (tuning runs).  (A
+    // warp-specialised variant of this kernel -- S1/S2 groups on named
+    // barriers, 608 threads -- measured 28.7k: DESIGN.md section 5.)
     static const bool early = [] {
         const char* e = getenv("LBM_K2_EARLY");
         return !(e && e[0] == '0');
     }();
-#define LBM_K2_TILE_CASE(TY, TZ)                                                     \
-    if constexpr (K2Cfg<T, TY, TZ>::FITS) {                                          \
-        if (early)                                                                   \
+#define LBM_K2_TILE_CASE(TY, TZ)                                                         \
+    if constexpr (K2Cfg<T, TY, TZ>::FITS) {                                              \
+        if (early)                                                                       \
             return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true>(A, B, P, xbeg, nxs, s) \
                        : launch_k2_impl<T, BC_CAVITY, TY, TZ, true>(A, B, P, xbeg, nxs, s);  \
-        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, false>(A, B, P, xbeg, nxs, s)   \
-                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, false>(A, B, P, xbeg, nxs, s);    \
-    } else {                                                                         \
-        return cudaErrorInvalidConfiguration;                                        \
+        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, false>(A, B, P, xbeg, nxs, s)    \
+                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, false>(A, B, P, xbeg, nxs, s);     \
+    } else {                                                                             \
+        return cudaErrorInvalidConfiguration;                                            \
     }
     switch (tile_choice(sizeof(T))) {
         case 1: LBM_K2_TILE_CASE(8, 32);
