@@ -192,7 +192,9 @@ lbm_status lbm_plan_halo(int nx, int ny, int nz, lbm_dtype dtype, int bc, int ra
  * performed. */
 typedef struct {
     long long launches;        /* all kernel launches by this context */
-    long long sweep_launches;  /* timed K1/K2 launches since lbm_profile_reset */
+    long long sweep_launches;  /* timed sweeps since lbm_profile_reset: one record per sweep of
+                                  all of the context's slabs (with a halo exchange overlapped,
+                                  interior + edge launches and the wait between them) */
     double sweep_ms;           /* their summed event time */
     long long sweep_updates;   /* cell updates they performed */
     long long k2_launches, k1_launches;

@@ -219,6 +219,34 @@ K2_VARIANTS = [("LBM_K2R_CFG", v, 3) for v in ["8x32s0", "8x32s1", "8x16s0m2", "
     [("LBM_K2_TILE", v, 2) for v in ["8x32", "8x16", "16x16"]] + [("LBM_K2_EARLY", "0", 2), ("LBM_K2_CHUNK", "3", 2)]
 
 
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_overlapped_exchange_bitwise(overlap, tmp_path):
+    """The halo exchange overlapped with the interior sweep (comm stream +
+    interior/edge split, the NCCL default) and the serial exchange give the
+    bits of a single slab, for LOCAL slabs on one device and the periodic
+    self-wrap, K2 and K1 (odd step) sweeps, both dtypes."""
+    import subprocess
+    import sys
+    import os
+    script = tmp_path / "overlap.py"
+    script.write_text(
+        "import numpy as np, lbm_inputs as li, paper_2208_05429_b200 as lbm\n"
+        "for bc in (lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC):\n"
+        "  for dims, slabs in [((48, 12, 40), 4), ((24, 9, 33), 2), ((12, 8, 32), 1), ((16, 8, 32), 4)]:\n"
+        "    for dt in ('f64', 'f32'):\n"
+        "      f0 = li.random_populations(43, *dims); r = []\n"
+        "      for s in (1, slabs):\n"
+        "        kw = dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=s) if s > 1 else {}\n"
+        "        with lbm.Lattice(*dims, 0.6, (0.05, 0, 0), dt, bc=bc, **kw) as lat:\n"
+        "          lat.set_populations(f0); lat.step(3); lat.step(2); r.append(lat.populations())\n"
+        "      assert np.array_equal(r[0], r[1]), (bc, dims, dt)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root, LBM_OVERLAP=overlap)
+    out = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
 @pytest.mark.parametrize("var,shape,kernel", K2_VARIANTS)
 def test_k2_variants_bitwise(var, shape, kernel, tmp_path):
     """Every compiled two-step variant (K2 tile TY x TZ, ring slack S, CTAs
