@@ -110,7 +110,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 __constant__ signed char c_slot_cx[kQ] = {-1, -1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1};
 __constant__ signed char c_slot_cy[kQ] = {0, -1, 1, 0, 0, 0, -1, 0, -1, -1, 1, 0, 1, 1, 0, 1, -1, 0, 0};
 __constant__ signed char c_slot_cz[kQ] = {0, 0, 0, -1, 1, 0, 0, -1, -1, 1, 0, 1, 1, -1, 0, 0, 0, 1, -1};
-__constant__ signed char c_slot_opp[kQ] = {14, 15, 16, 17, 18, 5, 10, 11, 12, 13, 6, 7, 8, 9, 0, 1, 2, 3, 4};
 
 __device__ __forceinline__ int wrapi(int v, int n) {
     v %= n;
@@ -208,26 +207,18 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         const bool rwall = BC == BC_CAVITY && p == g.nxl - 1 && g.right_wall;
         if (has1) {
             mbar_wait(&bar[s], uint32_t(c >> 1) & 1u);
-            if (edge_y || edge_z || lwall || rwall) {
-                // ---- fix-up of staged entries whose pull source leaves the domain ----
+            // Periodic edge tiles: staged entries whose source wraps are
+            // fetched here (CTA barrier).  Cavity wall links are resolved per
+            // thread in registers after the stage read (below), no barrier.
+            if (BC == BC_PERIODIC && (edge_y || edge_z)) {
+                // ---- fix-up of staged entries whose pull source wraps ----
                 auto fix = [&](int k, int aa, int bb) {
                     const int cx = c_slot_cx[k], cy = c_slot_cy[k], cz = c_slot_cz[k];
-                    const int fy = y0 - 1 + aa, fz = z0 - 1 + bb;
-                    const int sy = fy - cy, sz = fz - cz;
-                    const bool yz_out = sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz;
-                    if constexpr (BC == BC_CAVITY) {
-                        if (fy < 0 || fy >= g.ny || fz < 0 || fz >= g.nz) return;
-                        const bool out = yz_out || (cx == 1 && lwall) || (cx == -1 && rwall);
-                        if (!out) return;
-                        T v = A[cell_off(g, p, fy, fz) + (long long)c_slot_opp[k] * g.pq];
-                        if (cz == -1 && fz == g.nz - 1) v = v + P.lid[k];
-                        st[k * C::BOXE + aa * C::BW + bb + C::ZPAD - 1 - cz] = v;
-                    } else {
-                        if (!yz_out) return;
-                        st[k * C::BOXE + aa * C::BW + bb + C::ZPAD - 1 - cz] =
-                            A[(long long)(p - cx + 2) * g.px + (long long)k * g.pq +
-                              (long long)wrapi(sy, g.ny) * g.nzp + wrapi(sz, g.nz)];
-                    }
+                    const int sy = y0 - 1 + aa - cy, sz = z0 - 1 + bb - cz;
+                    if (sy >= 0 && sy < g.ny && sz >= 0 && sz < g.nz) return;
+                    st[k * C::BOXE + aa * C::BW + bb + C::ZPAD - 1 - cz] =
+                        A[(long long)(p - cx + 2) * g.px + (long long)k * g.pq +
+                          (long long)wrapi(sy, g.ny) * g.nzp + wrapi(sz, g.nz)];
                 };
                 // rows / columns whose sources can leave the domain
                 const int rlo = min(max(2 - y0, 0), C::HY), rhi = min(max(g.ny - y0, rlo), C::HY);
@@ -243,17 +234,6 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 for (int idx = tid; idx < n_cols; idx += C::NT) {
                     const int k = idx / (ngr * nbc), r = (idx / nbc) % ngr, cc = idx % nbc;
                     fix(k, rlo + r, cc < clo ? cc : chi + (cc - clo));
-                }
-                if (lwall || rwall) {  // the directions pulling through an x wall, interior entries
-                    const int ngc = C::HZ - nbc;
-                    const int ngroups = (lwall ? 1 : 0) + (rwall ? 1 : 0);
-                    const int n_x = ngroups * 5 * ngr * ngc;
-                    for (int idx = tid; idx < n_x; idx += C::NT) {
-                        const int j = idx / (ngr * ngc);  // 0..4 first group, 5..9 second
-                        const int k = (lwall && j < 5) ? kSlotP0 + j : (j % 5);
-                        const int r = (idx / ngc) % ngr, cc = idx % ngc;
-                        fix(k, rlo + r, clo + cc);
-                    }
                 }
                 __syncthreads();
             }
@@ -272,6 +252,34 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                     constexpr int k = decltype(kc)::value;
                     fs[slot_dir(k)] = sp[k * C::BOXE - can_cz(slot_dir(k))];
                 });
+                if constexpr (BC == BC_CAVITY) {
+                    // Wall links (source beyond a wall):
+                    // the staged entry (TMA zero fill, or a cell beyond the x
+                    // wall) is replaced by the cell's own opposite population
+                    // (+ lid), per thread -- the arithmetic of pull_cell().
+                    if ((edge_tile || lwall || rwall) && q_in) {
+                        const long long self = cell_off(g, p, qy, qz);
+                        static_for<0, kQ>([&](auto kc) {
+                            constexpr int k = decltype(kc)::value;
+                            constexpr int i = slot_dir(k);
+                            constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
+                            bool wall = false;
+                            if constexpr (cx == 1) wall = wall || lwall;
+                            if constexpr (cx == -1) wall = wall || rwall;
+                            if constexpr (cy == 1) wall = wall || qy == 0;
+                            if constexpr (cy == -1) wall = wall || qy == g.ny - 1;
+                            if constexpr (cz == 1) wall = wall || qz == 0;
+                            if constexpr (cz == -1) wall = wall || qz == g.nz - 1;
+                            if (wall) {
+                                T v = A[self + (long long)slot_opp(k) * g.pq];
+                                if constexpr (cz == -1) {
+                                    if (qz == g.nz - 1) v = v + P.lid[k];
+                                }
+                                fs[i] = v;
+                            }
+                        });
+                    }
+                }
             }
         };
         if constexpr (EARLY) {

@@ -1,0 +1,7 @@
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "k2_equals_k1 or local_slabs or overlapped" 2>&1 | tail -1
+SB="timeout 300 python tools/sweep_bench.py --dims 1024,512,512 --steps 10 --reps 2"
+$SB --dtype f64 --kernel k2 --tag k2
+$SB --dtype f32 --kernel k2 --tag k2
+$SB --dtype f64 --kernel k1 --tag k1
+$SB --dtype f64 --kernel k2 --bc periodic --tag k2-per
