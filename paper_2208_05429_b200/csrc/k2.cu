@@ -4,26 +4,32 @@
 // the second collide").
 //
 // Each CTA owns an output tile T of TY x TZ cells in the (y, z) plane and
-// marches along x over a chunk of planes (the paper's X-outermost order,
-// PAPER.md:335).  Per input plane p:
+// marches along x over a chunk of <= 64 planes (the paper's X-outermost
+// order; short chunks keep co-resident CTAs within a few planes
+// of each other, so the halo rows one CTA stages are still in L2 for its
+// neighbours).  Per input plane p:
 //   1. TMA stages f(t) on the tile plus a one-cell halo T+1: one box per
 //      direction, its origin shifted by -c_i, so the TMA unit performs the
-//      pull-stream (19 cp.async.bulk.tensor per plane, one mbarrier,
-//      double-buffered, two planes in flight).  Boxes that leave the domain
-//      are patched (bounce-back + lid, or periodic wrap) by a lean fix-up pass
-//      that only edge tiles and wall planes run.
+//      y part of the pull-stream (19 cp.async.bulk.tensor per plane, one
+//      mbarrier, double-buffered).  Each thread reads its 19 values into
+//      registers, then ONE block barrier frees the buffer and the TMA of
+//      plane p+2 is issued before any collision, so every load has two
+//      compute phases to land.  Entries whose source lies beyond a wall
+//      (bounce-back + lid) or wraps (periodic) are replaced per thread in
+//      registers with an ordinary load -- no CTA-wide fix-up pass.
 //   2. Step 1: every cell of T+1 collides (BGK, registers) and PUSHES its
 //      post-collision populations into a destination-indexed SMEM ring:
 //      direction i goes to the cell it streams to, (p + c_x, y + c_y, z + c_z).
 //      Wall links are resolved at the same time (bounce-back + lid into the
 //      cell's own slot), so the ring holds exactly f(t+1) of the tile.
-//   3. Step 2: once plane p has pushed, plane p-1 of the ring is complete;
-//      its cells collide again and store f*(t+1) to HBM with coalesced
-//      streaming stores.
+//   3. Step 2 of destination plane p-2 (complete since this iteration's
+//      barrier) runs in the same phase: a thread's step-2 cell and step-1
+//      cell collide as two interleaved dependency chains (bgk_collide2), and
+//      f*(t+1) leaves with coalesced streaming stores.
 // The ring keeps, per destination plane, only the populations still to
-// arrive: c_x = -1 group (5) x 2 planes, c_x = 0 (9) x 2, c_x = +1 (5) x 3.
+// arrive: c_x = -1 group (5) x 2 planes, c_x = 0 (9) x 3, c_x = +1 (5) x 4.
 // Every population therefore crosses HBM once per two steps (plus the halo
-// re-reads, which hit L2 when neighbouring tiles march in step).
+// re-reads that miss L2: 1.13-1.18x the algorithmic reads, ncu).
 //
 // The arithmetic is the same bgk_collide()/pull rules as K1 (d3q19.cuh), so
 // K2 == K1 o K1 bit for bit (tests/test_gpu_parity.py).
@@ -105,11 +111,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
-
-// slot-order direction tables for the (runtime-indexed) fix-up path
-__constant__ signed char c_slot_cx[kQ] = {-1, -1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1};
-__constant__ signed char c_slot_cy[kQ] = {0, -1, 1, 0, 0, 0, -1, 0, -1, -1, 1, 0, 1, 1, 0, 1, -1, 0, 0};
-__constant__ signed char c_slot_cz[kQ] = {0, 0, 0, -1, 1, 0, 0, -1, -1, 1, 0, 1, 1, -1, 0, 0, 0, 1, -1};
 
 __device__ __forceinline__ int wrapi(int v, int n) {
     v %= n;
@@ -207,36 +208,6 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         const bool rwall = BC == BC_CAVITY && p == g.nxl - 1 && g.right_wall;
         if (has1) {
             mbar_wait(&bar[s], uint32_t(c >> 1) & 1u);
-            // Periodic edge tiles: staged entries whose source wraps are
-            // fetched here (CTA barrier).  Cavity wall links are resolved per
-            // thread in registers after the stage read (below), no barrier.
-            if (BC == BC_PERIODIC && (edge_y || edge_z)) {
-                // ---- fix-up of staged entries whose pull source wraps ----
-                auto fix = [&](int k, int aa, int bb) {
-                    const int cx = c_slot_cx[k], cy = c_slot_cy[k], cz = c_slot_cz[k];
-                    const int sy = y0 - 1 + aa - cy, sz = z0 - 1 + bb - cz;
-                    if (sy >= 0 && sy < g.ny && sz >= 0 && sz < g.nz) return;
-                    st[k * C::BOXE + aa * C::BW + bb + C::ZPAD - 1 - cz] =
-                        A[(long long)(p - cx + 2) * g.px + (long long)k * g.pq +
-                          (long long)wrapi(sy, g.ny) * g.nzp + wrapi(sz, g.nz)];
-                };
-                // rows / columns whose sources can leave the domain
-                const int rlo = min(max(2 - y0, 0), C::HY), rhi = min(max(g.ny - y0, rlo), C::HY);
-                const int clo = min(max(2 - z0, 0), C::HZ), chi = min(max(g.nz - z0, clo), C::HZ);
-                const int nbr = rlo + (C::HY - rhi), nbc = clo + (C::HZ - chi);
-                const int n_rows = kQ * nbr * C::HZ;
-                for (int idx = tid; idx < n_rows; idx += C::NT) {
-                    const int k = idx / (nbr * C::HZ), r = (idx / C::HZ) % nbr, bb = idx % C::HZ;
-                    fix(k, r < rlo ? r : rhi + (r - rlo), bb);
-                }
-                const int ngr = C::HY - nbr;  // rows not covered above
-                const int n_cols = kQ * ngr * nbc;
-                for (int idx = tid; idx < n_cols; idx += C::NT) {
-                    const int k = idx / (ngr * nbc), r = (idx / nbc) % ngr, cc = idx % nbc;
-                    fix(k, rlo + r, cc < clo ? cc : chi + (cc - clo));
-                }
-                __syncthreads();
-            }
         }
         // Read this thread's staged f(t) into registers, then ONE barrier:
         // the stage buffer is free and the TMA of plane p+2 is issued before
@@ -252,6 +223,22 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                     constexpr int k = decltype(kc)::value;
                     fs[slot_dir(k)] = sp[k * C::BOXE - can_cz(slot_dir(k))];
                 });
+                if constexpr (BC == BC_PERIODIC) {
+                    // Sources that wrap (outside [0,ny) x [0,nz)): fetched per
+                    // thread from the wrapped cell (TMA zero-filled them); no
+                    // CTA-wide fix-up pass (measured +9% over one).
+                    if ((edge_y || edge_z) && act1) {
+                        static_for<0, kQ>([&](auto kc) {
+                            constexpr int k = decltype(kc)::value;
+                            constexpr int i = slot_dir(k);
+                            constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
+                            const int sy = qy - cy, sz = qz - cz;
+                            if (sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz)
+                                fs[i] = A[(long long)(p - cx + 2) * g.px + (long long)k * g.pq +
+                                          (long long)wrapi(sy, g.ny) * g.nzp + wrapi(sz, g.nz)];
+                        });
+                    }
+                }
                 if constexpr (BC == BC_CAVITY) {
                     // Wall links (source beyond a wall):
                     // the staged entry (TMA zero fill, or a cell beyond the x
