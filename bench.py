@@ -324,6 +324,19 @@ def main():
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "MLUPS", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
 
+    # roofline.traffic: measured DRAM bytes per sweep launch from the committed
+    # ncu capture of this workload/dtype/kernel (profiles/r01_traffic.json), if any
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+        t = tj.get(cfg.name, {}).get(dominant, {}).get(args.dtype) if world == 1 else None
+        if t:
+            traffic = {"bytes_per_launch": t["read"] + t["write"], "read": t["read"], "write": t["write"],
+                       "x_algorithmic": round((t["read"] + t["write"]) / bytes_per_launch, 3),
+                       "source": "profiles/r01_traffic.json (ncu --set full, same workload)"}
+    except (OSError, ValueError, KeyError):
+        traffic = None
+
     if rank == 0:
         mlups_bytes = 2 * 19 * es  # BASELINE.json:5 roofline: MLUPS x single-step bytes / peak
         line = {
@@ -338,7 +351,11 @@ def main():
                        "l2": f"inputs larger than L2: {cells_local * 19 * es / 1e9:.1f} GB per lattice copy per GPU"},
             "mlups_per_gpu": round(value / world, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None, "kernel": dominant,
+                         "frac": round(achieved / peak, 4),
+                         # measured DRAM bytes per launch over the same live launch time (GB/s, vs achieved)
+                         "traffic": None if traffic is None else
+                         round(traffic["bytes_per_launch"] / (avg_launch_ms * 1e-3) / 1e9, 1),
+                         "traffic_detail": traffic, "kernel": dominant,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": round(avg_launch_ms, 4), "peak_source": peak_src,
                          "sweep_share_of_step": None if sweep_share is None else round(sweep_share, 4),
