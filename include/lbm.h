@@ -82,7 +82,19 @@ typedef enum {
  * AUTO = K2, falling back to K1 pairs where no two-step variant fits; an
  * explicit K2/K2_REG on such a slab gives EINVAL from lbm_step.  Results are
  * bitwise identical whichever kernel runs. */
-typedef enum { LBM_KERNEL_AUTO = 0, LBM_KERNEL_K1 = 1, LBM_KERNEL_K2 = 2, LBM_KERNEL_K2_REG = 3 } lbm_kernel;
+typedef enum {
+    LBM_KERNEL_AUTO = 0,
+    LBM_KERNEL_K1 = 1,
+    LBM_KERNEL_K2 = 2,
+    LBM_KERNEL_K2_REG = 3,
+    /* Single-copy in-place storage, the AA pattern (
+     * the paper's one-lattice swap): one lattice
+     * buffer instead of two (half the memory), alternating an in-place
+     * collide-and-revert step with a gather/scatter step; one step per HBM
+     * pass (K1's bytes).  Needs world == 1 and local_slabs == 1 (EINVAL
+     * otherwise).  Bitwise identical to K1. */
+    LBM_KERNEL_AA = 4
+} lbm_kernel;
 
 /* Halo transport between X-slabs (PAPER.md:336 X-only partition).
  *  NONE   world == 1 and local_slabs == 1 (periodic x wraps onto itself)

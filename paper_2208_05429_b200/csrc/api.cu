@@ -93,6 +93,11 @@ struct lbm_ctx {
     cudaStream_t comm_stream = nullptr;  // highest priority: its NCCL kernels win free SMs
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     bool overlap = true;
+    // single-copy AA storage (LBM_KERNEL_AA, aa.cu): buf[0] only, plus a
+    // staging buffer for host transfers; aa_odd = the next step is odd
+    bool aa = false, aa_odd = false;
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
     ncclComm_t comm = nullptr;
     size_t esize = 8;
     int* d_flag = nullptr;
@@ -232,7 +237,7 @@ bool has_neighbours(const lbm_ctx* c) {
 }
 
 lbm_status ensure_ghosts(lbm_ctx* c) {
-    if (c->ghosts_valid || !has_neighbours(c)) {
+    if (c->ghosts_valid || !has_neighbours(c) || c->aa) {  // AA wraps x in the kernels
         c->ghosts_valid = true;
         return LBM_OK;
     }
@@ -274,8 +279,30 @@ lbm_status prof_end(lbm_ctx* c, size_t slot, long long updates) {
 }
 
 // --------------------------------------------------------------- engine --
+// single-copy AA storage: alternate the in-place even / odd steps (aa.cu)
+template <typename T>
+lbm_status run_steps_aa(lbm_ctx* c, long n) {
+    Slab& s = c->slabs[0];
+    const StepParams<T> P = make_params<T>(c, s);
+    for (; n > 0; --n) {
+        size_t slot = 0;
+        lbm_status st = prof_begin(c, slot);
+        if (st != LBM_OK) return st;
+        cudaError_t e = launch_aa_step<T>(static_cast<T*>(s.buf[0]), P, c->aa_odd, c->stream);
+        if (e != cudaSuccess) return fail(c, LBM_ECUDA, "AA step launch failed: %s", cudaGetErrorString(e));
+        c->launches++;
+        c->k1_launches++;
+        st = prof_end(c, slot, (long long)s.g.nxl * s.g.ny * s.g.nz);
+        if (st != LBM_OK) return st;
+        c->aa_odd = !c->aa_odd;
+        c->t += 1;
+    }
+    return LBM_OK;
+}
+
 template <typename T>
 lbm_status run_steps(lbm_ctx* c, long n) {
+    if (c->aa) return run_steps_aa<T>(c, n);
     // AUTO and K2: the TMA-staged two-step sweep (k2.cu) where the TMA
     // descriptor can describe the slab, else the cp.async-staged one (K2R,
     // k2r.cu); K2_REG forces K2R.  AUTO falls back to K1 pairs when neither
@@ -372,6 +399,13 @@ lbm_status validate_device(lbm_ctx* c, const double* v, long long n, bool positi
 // f(t0) canonical in buffer `which` of every slab (own planes) -> state.
 template <typename T>
 lbm_status finish_init(lbm_ctx* c, int canon) {
+    if (c->aa) {  // canonical f(t0) in buf[0] IS the at-rest AA state
+        c->cur = 0;
+        c->aa_odd = false;
+        c->initialized = true;
+        c->t = 0;
+        return LBM_OK;
+    }
     // the inverse stream reads the neighbours' canonical planes
     if (has_neighbours(c)) {
         lbm_status st = exchange(c, canon, c->stream);
@@ -391,7 +425,48 @@ lbm_status finish_init(lbm_ctx* c, int canon) {
 }
 
 template <typename T>
+lbm_status init_eq_aa(lbm_ctx* c, const double* rho, const double* u, bool host) {
+    const long long plane = (long long)c->ny * c->nz;
+    Slab& s = c->slabs[0];
+    T* F = static_cast<T*>(s.buf[0]);
+    if (!host) {
+        CK(launch_k0_equilibrium<T>(rho, u, F, s.g, c->stream));
+        c->launches++;
+        return finish_init<T>(c, 0);
+    }
+    // planes per chunk: 32 B (rho + u) per cell in the staging buffer
+    const int cap = int(std::max<long long>(1, (long long)(c->stage_bytes / (4 * sizeof(double))) / plane));
+    double* stage = static_cast<double*>(c->stage);
+    for (int xb = 0; xb < s.g.nxl; xb += cap) {
+        const int nxc = std::min(cap, s.g.nxl - xb);
+        const long long cells = (long long)nxc * plane;
+        const double* dr = nullptr;
+        const double* du = nullptr;
+        if (rho) {
+            CK(cudaMemcpyAsync(stage, rho + (long long)xb * plane, cells * sizeof(double), cudaMemcpyHostToDevice,
+                               c->stream));
+            dr = stage;
+        }
+        if (u) {
+            CK(cudaMemcpyAsync(stage + cells, u + 3 * (long long)xb * plane, 3 * cells * sizeof(double),
+                               cudaMemcpyHostToDevice, c->stream));
+            du = stage + cells;
+        }
+        int flag = 0;
+        lbm_status st;
+        if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
+        if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+        if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
+        if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+        CK(launch_k0_equilibrium<T>(dr, du, F, s.g, c->stream, xb, nxc));
+        c->launches++;
+    }
+    return finish_init<T>(c, 0);
+}
+
+template <typename T>
 lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
+    if (c->aa) return init_eq_aa<T>(c, rho, u, host);
     const long long plane = (long long)c->ny * c->nz;
     const int canon = c->cur;  // canonical f(t0) is built here, the state ends in the other buffer
     for (Slab& s : c->slabs) {
@@ -431,11 +506,14 @@ template <typename T>
 lbm_status set_pops(lbm_ctx* c, const double* f) {
     const long long plane = (long long)c->ny * c->nz;
     const long long proc_cells = (long long)c->nxl_proc * plane;
-    const int canon = c->cur ^ 1;  // import into the non-state buffer, stage in the state buffer
-    c->initialized = false;       // the state buffer is used as staging
+    // import into the non-state buffer, stage in the state buffer (AA: into
+    // the single buffer, staged in the staging buffer)
+    const int canon = c->aa ? 0 : c->cur ^ 1;
+    c->initialized = false;
     for (Slab& s : c->slabs) {
-        double* stage = static_cast<double*>(s.buf[canon ^ 1]);
-        const long long cap_planes = (long long)(s.plan.buffer_elems * c->esize) / (kQ * plane * sizeof(double));
+        double* stage = static_cast<double*>(c->aa ? c->stage : s.buf[canon ^ 1]);
+        const size_t stage_bytes = c->aa ? c->stage_bytes : size_t(s.plan.buffer_elems) * c->esize;
+        const long long cap_planes = (long long)stage_bytes / (kQ * plane * (long long)sizeof(double));
         for (int xb = 0; xb < s.g.nxl; xb += int(cap_planes)) {
             const int nxc = int(std::min<long long>(cap_planes, s.g.nxl - xb));
             const long long ccells = (long long)nxc * plane;
@@ -454,7 +532,38 @@ lbm_status set_pops(lbm_ctx* c, const double* f) {
 }
 
 template <typename T>
+lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
+    const long long plane = (long long)c->ny * c->nz;
+    Slab& s = c->slabs[0];
+    const StepParams<T> P = make_params<T>(c, s);
+    const T* F = static_cast<const T*>(s.buf[0]);
+    if (!host) {
+        CK(launch_aa_moments<T>(F, P, c->aa_odd, 0, s.g.nxl, rho, u, c->stream));
+        c->launches++;
+        return LBM_OK;
+    }
+    const int cap = int(std::max<long long>(1, (long long)(c->stage_bytes / (4 * sizeof(double))) / plane));
+    double* stage = static_cast<double*>(c->stage);
+    for (int xb = 0; xb < s.g.nxl; xb += cap) {
+        const int nxc = std::min(cap, s.g.nxl - xb);
+        const long long cells = (long long)nxc * plane;
+        CK(launch_aa_moments<T>(F, P, c->aa_odd, xb, nxc, rho ? stage : nullptr, u ? stage + cells : nullptr,
+                                c->stream));
+        c->launches++;
+        if (rho)
+            CK(cudaMemcpyAsync(rho + (long long)xb * plane, stage, cells * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
+        if (u)
+            CK(cudaMemcpyAsync(u + 3 * (long long)xb * plane, stage + cells, 3 * cells * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return LBM_OK;
+}
+
+template <typename T>
 lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
+    if (c->aa) return macro_aa<T>(c, rho, u, host);
     lbm_status st = ensure_ghosts(c);
     if (st != LBM_OK) return st;
     const long long plane = (long long)c->ny * c->nz;
@@ -495,13 +604,19 @@ lbm_status get_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, d
         const int a = std::max(bx, sx0), b = std::min(bx + lx, sx0 + s.g.nxl);
         if (a >= b) continue;
         const StepParams<T> P = make_params<T>(c, s);
-        double* stage = static_cast<double*>(s.buf[c->cur ^ 1]);
-        const long long cap_planes = (long long)(s.plan.buffer_elems * c->esize) / (kQ * bplane * sizeof(double));
+        double* stage = static_cast<double*>(c->aa ? c->stage : s.buf[c->cur ^ 1]);
+        const size_t stage_bytes = c->aa ? c->stage_bytes : size_t(s.plan.buffer_elems) * c->esize;
+        const long long cap_planes =
+            std::max<long long>(1, (long long)stage_bytes / (kQ * bplane * (long long)sizeof(double)));
         for (int xb = a; xb < b; xb += int(cap_planes)) {
             const int nxc = int(std::min<long long>(cap_planes, b - xb));
             const long long ccells = (long long)nxc * bplane;
-            CK(launch_k3_materialize<T>(static_cast<const T*>(s.buf[c->cur]), P, xb - sx0, by, bz, nxc, ly, lz, stage,
-                                        c->stream));
+            if (c->aa)
+                CK(launch_aa_materialize<T>(static_cast<const T*>(s.buf[0]), P, c->aa_odd, xb - sx0, by, bz, nxc,
+                                            ly, lz, stage, c->stream));
+            else
+                CK(launch_k3_materialize<T>(static_cast<const T*>(s.buf[c->cur]), P, xb - sx0, by, bz, nxc, ly, lz,
+                                            stage, c->stream));
             c->launches++;
             CK(cudaMemcpy2DAsync(out + (long long)(xb - bx) * bplane, bcells * sizeof(double), stage,
                                  ccells * sizeof(double), ccells * sizeof(double), kQ, cudaMemcpyDeviceToHost,
@@ -585,7 +700,9 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         return fail(c, LBM_EINVAL, "comm NCCL needs local_slabs == 1 and an nccl_id");
     if (o.comm == LBM_COMM_LOCAL && o.world != 1) return fail(c, LBM_EINVAL, "comm LOCAL needs world == 1");
     if (o.comm < LBM_COMM_NONE || o.comm > LBM_COMM_LOCAL) return fail(c, LBM_EINVAL, "bad comm %d", o.comm);
-    if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K2_REG) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_AA) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    if (o.kernel == LBM_KERNEL_AA && (o.world != 1 || o.local_slabs != 1))
+        return fail(c, LBM_EINVAL, "kernel AA (single-copy storage) needs world == 1 and local_slabs == 1");
     const int nslab_total = o.world * o.local_slabs;
     if (nx % nslab_total) return fail(c, LBM_EINVAL, "nx %d not divisible by %d slabs", nx, nslab_total);
     const int nxl = nx / nslab_total;
@@ -644,7 +761,7 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
             s.right = s.plan.right >= 0 ? s.plan.right - o.rank * sw : -1;
         }
         const size_t bytes = size_t(s.plan.buffer_elems) * c->esize;
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < (o.kernel == LBM_KERNEL_AA ? 1 : 2); ++b) {
             cudaError_t e = cudaMalloc(&s.buf[b], bytes);
             if (e != cudaSuccess) {
                 cudaGetLastError();
@@ -655,6 +772,18 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         }
     }
     if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess) return bail(fail(c, LBM_ENOMEM, "cudaMalloc flag"));
+    if (o.kernel == LBM_KERNEL_AA) {
+        // host transfers are staged plane-chunk by plane-chunk: >= one plane
+        // of 19 doubles, 64 MB or 1/16 of the lattice, whichever is larger
+        c->aa = true;
+        const size_t plane19 = size_t(kQ) * ny * nz * sizeof(double);
+        const size_t lattice = size_t(c->slabs[0].plan.buffer_elems) * c->esize;
+        c->stage_bytes = std::max({plane19, size_t(64) << 20, lattice / 16});
+        if (cudaMalloc(&c->stage, c->stage_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return bail(fail(c, LBM_ENOMEM, "cudaMalloc staging (%zu bytes)", c->stage_bytes));
+        }
+    }
     if (o.stream) {
         c->stream = static_cast<cudaStream_t>(o.stream);
     } else {
@@ -703,6 +832,7 @@ void lbm_destroy(lbm_ctx* c) {
         for (void* b : s.buf)
             if (b) cudaFree(b);
     if (c->d_flag) cudaFree(c->d_flag);
+    if (c->stage) cudaFree(c->stage);
     if (c->comm_stream) {
         cudaStreamSynchronize(c->comm_stream);
         cudaStreamDestroy(c->comm_stream);

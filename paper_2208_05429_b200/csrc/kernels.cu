@@ -37,12 +37,12 @@ __global__ void __launch_bounds__(256) k1_step(const T* __restrict__ A, T* __res
 // layout).  rho/u are double arrays [x][y][z] / [x][y][z][3] of the slab.
 template <typename T>
 __global__ void __launch_bounds__(256) k0_equilibrium(const double* __restrict__ rho, const double* __restrict__ u,
-                                                     T* __restrict__ C, SlabGeom g) {
+                                                     T* __restrict__ C, SlabGeom g, int xbeg) {
     const int z = blockIdx.x * 32 + threadIdx.x;
     const int y = blockIdx.y * 8 + threadIdx.y;
-    const int x = blockIdx.z;
+    const int x = xbeg + blockIdx.z;  // rho/u hold planes [xbeg, xbeg + gridDim.z)
     if (z >= g.nz || y >= g.ny) return;
-    const long long cell = ((long long)x * g.ny + y) * g.nz + z;
+    const long long cell = ((long long)blockIdx.z * g.ny + y) * g.nz + z;
     const T r = rho ? T(rho[cell]) : T(1);
     T ux = T(0), uy = T(0), uz = T(0);
     if (u) {
@@ -178,8 +178,11 @@ cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
 }
 
 template <typename T>
-cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, const SlabGeom& g, cudaStream_t s) {
-    k0_equilibrium<T><<<cell_grid(g.nz, g.ny, g.nxl), kBlock, 0, s>>>(rho, u, C, g);
+cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, const SlabGeom& g, cudaStream_t s,
+                                  int xbeg, int nxc) {
+    if (nxc < 0) nxc = g.nxl;
+    if (nxc == 0) return cudaSuccess;
+    k0_equilibrium<T><<<cell_grid(g.nz, g.ny, nxc), kBlock, 0, s>>>(rho, u, C, g, xbeg);
     return cudaGetLastError();
 }
 
@@ -221,7 +224,7 @@ cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int 
 #define LBM_INSTANTIATE(T)                                                                                   \
     template cudaError_t launch_k1<T>(const T*, T*, const StepParams<T>&, int, int, cudaStream_t);           \
     template cudaError_t launch_k0_equilibrium<T>(const double*, const double*, T*, const SlabGeom&,         \
-                                                  cudaStream_t);                                             \
+                                                  cudaStream_t, int, int);                                   \
     template cudaError_t launch_k0_unstream<T>(const T*, T*, const StepParams<T>&, cudaStream_t);            \
     template cudaError_t launch_k0_import<T>(const double*, T*, const SlabGeom&, int, int, cudaStream_t);    \
     template cudaError_t launch_k3_materialize<T>(const T*, const StepParams<T>&, int, int, int, int, int,   \

@@ -23,8 +23,22 @@ bool k2r_supported(const SlabGeom& g);
 template <typename T>
 cudaError_t launch_k2r(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s);
 
+// canonical feq of planes [xbeg, xbeg + nxc) (nxc < 0: the whole slab); rho/u
+// point at the first of those planes
 template <typename T>
-cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, const SlabGeom& g, cudaStream_t s);
+cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, const SlabGeom& g, cudaStream_t s,
+                                  int xbeg = 0, int nxc = -1);
+
+// Single-copy AA storage (aa.cu): one in-place step (odd = the gather/scatter
+// half), and the canonical f / moments of either phase.
+template <typename T>
+cudaError_t launch_aa_step(T* F, const StepParams<T>& P, bool odd, cudaStream_t s);
+template <typename T>
+cudaError_t launch_aa_materialize(const T* F, const StepParams<T>& P, bool odd, int x0, int y0, int z0, int lx,
+                                  int ly, int lz, double* out, cudaStream_t s);
+template <typename T>
+cudaError_t launch_aa_moments(const T* F, const StepParams<T>& P, bool odd, int xbeg, int nxc, double* rho,
+                              double* u, cudaStream_t s);
 template <typename T>
 cudaError_t launch_k0_unstream(const T* C, T* A, const StepParams<T>& P, cudaStream_t s);
 template <typename T>

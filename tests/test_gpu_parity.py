@@ -289,3 +289,68 @@ def test_k2_local_slabs_bitwise(bc):
             outs.append(lat.populations())
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+
+
+AA_DIMS = [(1, 8, 32), (3, 9, 33), (5, 17, 31), (7, 8, 32), (12, 24, 96)]
+
+
+@pytest.mark.parametrize("dims", AA_DIMS)
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("lid", [(0.0, 0.0, 0.0), LID])
+def test_aa_single_copy_equals_k1(dims, bc, dtype, lid):
+    """Single-copy AA storage: after every step count
+    (both storage phases) the canonical populations and the moments equal
+    K1's, and match the oracle; ragged tiles, every wall, the lid, periodic
+    wraps (one-plane x included).  Bit for bit without a lid; with the lid
+    K1's pull storage holds f(t0) - lid and adds it back on read (S(S^-1 f)
+    rounds at the lid cells, ~1 ulp) while AA stores f(t0) itself, so there
+    the two agree to rounding (and both with the oracle)."""
+    if bc == lbm.LBM_BC_PERIODIC and (dims[0] < 2 or lid != LID):
+        pytest.skip("periodic needs >= 2 planes; the lid is a cavity feature")
+    f0 = li.random_populations(47, *dims)
+    exact = lid == (0.0, 0.0, 0.0) or bc == lbm.LBM_BC_PERIODIC
+    with lbm.Lattice(*dims, 0.6, lid, dtype, bc=bc, kernel=lbm.LBM_KERNEL_K1) as ref, \
+            lbm.Lattice(*dims, 0.6, lid, dtype, bc=bc, kernel=lbm.LBM_KERNEL_AA) as aa:
+        ref.set_populations(f0)
+        aa.set_populations(f0)
+        assert np.array_equal(aa.populations(), f0 if dtype == "f64" else f0.astype(np.float32).astype(np.float64))
+        for n in (1, 1, 2, 1):
+            ref.step(n)
+            aa.step(n)
+            assert aa.time == ref.time
+            a, b = aa.populations(), ref.populations()
+            r1, u1 = ref.macroscopic()
+            r2, u2 = aa.macroscopic()
+            if exact:
+                assert np.array_equal(a, b)
+                assert np.array_equal(r1, r2) and np.array_equal(u1, u2)
+            else:
+                assert relerr_floor(a, b) <= (1e-14 if dtype == "f64" else 1e-6)
+        got = aa.populations()
+    assert relerr_floor(got, oracle.run(f0, bc, 0.6, lid, 5)) <= TOL[dtype]
+
+
+def test_aa_config2_init_equilibrium_and_errors():
+    """AA from lbm_init_equilibrium (host and device inputs) on the config-2
+    cavity (64^3, lid) for 30 steps agrees with K1 and the oracle; host and
+    device inputs give identical bits; AA refuses multi-slab contexts."""
+    cfg = li.CONFIGS[2]
+    rho, u = li.init_fields(cfg)
+    outs = []
+    for kernel in (lbm.LBM_KERNEL_K1, lbm.LBM_KERNEL_AA):
+        with lbm.Lattice(cfg.nx, cfg.ny, cfg.nz, cfg.tau, cfg.u_lid, "f64", bc=cfg.bc, kernel=kernel) as lat:
+            lat.init_equilibrium(rho, u)
+            lat.step(30)
+            outs.append((lat.populations(), *lat.macroscopic()))
+    assert relerr(outs[1][0], outs[0][0]) <= 1e-14
+    ref = oracle.run(oracle.init_equilibrium(cfg.nx, cfg.ny, cfg.nz, rho, u), cfg.bc, cfg.tau, cfg.u_lid, 30)
+    assert relerr(outs[1][0], ref) <= 1e-12
+    with lbm.Lattice(cfg.nx, cfg.ny, cfg.nz, cfg.tau, cfg.u_lid, "f64", bc=cfg.bc, kernel=lbm.LBM_KERNEL_AA) as lat:
+        rd = torch.from_numpy(rho).cuda()
+        ud = torch.from_numpy(u).cuda()
+        lbm.lbm_init_equilibrium_device(lat.ctx, rd, ud)
+        lat.step(30)
+        assert np.array_equal(lat.populations(), outs[1][0])
+    with pytest.raises(lbm.LbmError):
+        lbm.Lattice(16, 8, 8, 0.6, LID, "f64", kernel=lbm.LBM_KERNEL_AA, comm=lbm.LBM_COMM_LOCAL, local_slabs=2)
