@@ -143,8 +143,19 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const int p_last = (xe == g.nxl && BC == BC_CAVITY && g.right_wall) ? g.nxl - 1 : xe;
 
     const int tid = threadIdx.x;
-    // step-1 cell of this thread: box coordinates (a, b), cell (p, qy, qz)
-    const int a = tid / C::HZ, b = tid % C::HZ;
+    // step-1 cell of this thread: box coordinates (a, b), cell (p, qy, qz).
+    // Threads [0, HY*TZ) take the TZ interior columns row by row (a warp =
+    // 32 consecutive cells of one row: conflict-free stage reads and ring
+    // pushes when TZ = 32); the next 2*HY threads take the two halo columns.
+    int a, b;
+    if (tid < C::HY * TZ) {
+        a = tid / TZ;
+        b = 1 + tid % TZ;
+    } else {
+        const int j = tid - C::HY * TZ;
+        a = j >> 1;
+        b = (j & 1) ? TZ + 1 : 0;
+    }
     const bool act1 = tid < C::HY * C::HZ;
     const int qy = y0 - 1 + a, qz = z0 - 1 + b;
     const bool q_in = act1 && (BC == BC_PERIODIC || (qy >= 0 && qy < g.ny && qz >= 0 && qz < g.nz));
