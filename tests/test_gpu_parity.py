@@ -354,3 +354,27 @@ def test_aa_config2_init_equilibrium_and_errors():
         assert np.array_equal(lat.populations(), outs[1][0])
     with pytest.raises(lbm.LbmError):
         lbm.Lattice(16, 8, 8, 0.6, LID, "f64", kernel=lbm.LBM_KERNEL_AA, comm=lbm.LBM_COMM_LOCAL, local_slabs=2)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_nccl_transport_world1_periodic_bitwise(dtype):
+    """The NCCL halo path on hardware: a one-rank communicator on a periodic
+    box sends its x-halo spans to itself (ncclSend/ncclRecv to self in one
+    group), on the high-priority comm stream overlapped with the interior
+    sweep (the NCCL default), for K2 and K1 (odd) sweeps -- bitwise equal to
+    the in-process wrap, and to the oracle."""
+    dims = (24, 10, 36)
+    f0 = li.random_populations(53, *dims)
+    try:
+        uid = lbm.lbm_nccl_unique_id()
+    except lbm.LbmError as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    outs = []
+    for comm, kw in [(lbm.LBM_COMM_NONE, {}), (lbm.LBM_COMM_NCCL, {"nccl_id": uid})]:
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=lbm.LBM_BC_PERIODIC, comm=comm, **kw) as lat:
+            lat.set_populations(f0)
+            lat.step(3)
+            lat.step(2)
+            outs.append(lat.populations())
+    assert np.array_equal(outs[0], outs[1])
+    assert relerr_floor(outs[1], oracle.run(f0, lbm.LBM_BC_PERIODIC, 0.6, LID, 5)) <= TOL[dtype]
