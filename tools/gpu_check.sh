@@ -1,3 +1,4 @@
+# Standard GPU check (run under gpurun): build, all GPU tests, sweep micro-bench; "bench" adds a bench.py line.
 # standard GPU check: build, all GPU tests, sweep micro-bench, sustained bench (no CPU leg)
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/t_all.log 2>&1; tail -2 gpurun_out/t_all.log
