@@ -27,25 +27,31 @@ namespace lbm {
 
 namespace {
 
-__device__ __forceinline__ int wrap1(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
-
-// Offset of cell (x, y, z), periodic wrap applied to out-of-range coordinates.
-template <int BC>
-__device__ __forceinline__ long long aa_cell(const SlabGeom& g, int x, int y, int z) {
-    if constexpr (BC == BC_PERIODIC) {
-        x = wrap1(x, g.nxl);
-        y = wrap1(y, g.ny);
-        z = wrap1(z, g.nz);
+// Element offset of F[x + d][slot] for the neighbour d = +-c of cell
+// (x, y, z) along a compile-time direction, or -1 if that neighbour lies
+// beyond a cavity wall.  Only the axes the direction moves along are
+// tested (periodic: wrapped), like pull_src() for K1.
+template <int BC, int dx, int dy, int dz>
+__device__ __forceinline__ long long aa_nbr(const SlabGeom& g, int x, int y, int z, int slot) {
+    int nx_ = x + dx, ny_ = y + dy, nz_ = z + dz;
+    if constexpr (BC == BC_CAVITY) {
+        bool out = false;
+        if constexpr (dx == -1) out = out || x == 0;
+        if constexpr (dx == 1) out = out || x == g.nxl - 1;
+        if constexpr (dy == -1) out = out || y == 0;
+        if constexpr (dy == 1) out = out || y == g.ny - 1;
+        if constexpr (dz == -1) out = out || z == 0;
+        if constexpr (dz == 1) out = out || z == g.nz - 1;
+        if (out) return -1;
+    } else {
+        if constexpr (dx == -1) nx_ = x == 0 ? g.nxl - 1 : nx_;
+        if constexpr (dx == 1) nx_ = x == g.nxl - 1 ? 0 : nx_;
+        if constexpr (dy == -1) ny_ = y == 0 ? g.ny - 1 : ny_;
+        if constexpr (dy == 1) ny_ = y == g.ny - 1 ? 0 : ny_;
+        if constexpr (dz == -1) nz_ = z == 0 ? g.nz - 1 : nz_;
+        if constexpr (dz == 1) nz_ = z == g.nz - 1 ? 0 : nz_;
     }
-    return cell_off(g, x, y, z);
-}
-
-// Does the link from cell (x,y,z) along -c (the pull source) or +c (the push
-// target) leave a cavity?
-template <int BC>
-__device__ __forceinline__ bool aa_out(const SlabGeom& g, int x, int y, int z) {
-    if constexpr (BC == BC_PERIODIC) return false;
-    return x < 0 || x >= g.nxl || y < 0 || y >= g.ny || z < 0 || z >= g.nz;
+    return cell_off(g, nx_, ny_, nz_) + (long long)slot * g.pq;
 }
 
 // canonical f(x, t) from F: at rest (even) or after an even step (odd)
@@ -62,13 +68,13 @@ __device__ __forceinline__ void aa_gather(const T* __restrict__ F, const StepPar
         if (!odd) {
             v = F[self + (long long)k * g.pq];
         } else {
-            const int sx = x - cx, sy = y - cy, sz = z - cz;
-            if (!aa_out<BC>(g, sx, sy, sz)) {
-                v = F[aa_cell<BC>(g, sx, sy, sz) + (long long)slot_opp(k) * g.pq];
+            const long long src = aa_nbr<BC, -cx, -cy, -cz>(g, x, y, z, slot_opp(k));
+            if (src >= 0) {
+                v = F[src];
             } else {
                 v = F[self + (long long)k * g.pq];
                 if constexpr (BC == BC_CAVITY && cz == -1) {
-                    if (sz >= g.nz) v = v + P.lid[k];
+                    if (z == g.nz - 1) v = v + P.lid[k];
                 }
             }
         }
@@ -113,9 +119,9 @@ __global__ void __launch_bounds__(256) k_aa_odd(T* __restrict__ F, StepParams<T>
         constexpr int k = decltype(kc)::value;
         constexpr int i = slot_dir(k);
         constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
-        const int tx = x + cx, ty = y + cy, tz = z + cz;
-        if (!aa_out<BC>(g, tx, ty, tz)) {
-            F[aa_cell<BC>(g, tx, ty, tz) + (long long)k * g.pq] = f[i];
+        const long long dst = aa_nbr<BC, cx, cy, cz>(g, x, y, z, k);
+        if (dst >= 0) {
+            F[dst] = f[i];
         } else {
             // f*_i leaves through a wall: it is population opp(i) of this cell
             // at the next step, plus the lid term of that link (its source,
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(256) k_aa_odd(T* __restrict__ F, StepParams<T>
             constexpr int ko = slot_opp(k);
             T v = f[i];
             if constexpr (BC == BC_CAVITY && cz == 1) {
-                if (tz >= g.nz) v = v + P.lid[ko];
+                if (z == g.nz - 1) v = v + P.lid[ko];
             }
             F[self + (long long)ko * g.pq] = v;
         }
