@@ -476,10 +476,12 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     // x chunks of at most kMaxChunk planes: co-resident CTAs start a chunk
     // together and stay within a few planes of each other, so the halo rows
     // and columns one CTA stages are still in L2 when its neighbours stage
-    // them (measured on 1024x512x512 fp64: chunk 48 33.6k MLUPS, 96 30.8k,
-    // whole-slab 27k).  Among those, fill whole waves of the machine; each
-    // chunk re-computes ~2.5 planes of step 1.
-    constexpr int kMaxChunk = 64;
+    // them (DRAM reads 1.13x / 1.19x / 1.38x / 1.49x the algorithmic bytes
+    // at 32 / 64 / 128 / 512 planes, 512^3 fp64; 1024x512x512 fp64 equal
+    // within noise at 32-64 planes, 256^3 periodic 5% faster at 32 than 64).
+    // Among those, fill whole waves of the machine; each chunk re-computes
+    // ~2.5 planes of step 1.
+    constexpr int kMaxChunk = 32;
     int best = 1;
     double best_cost = 1e300;
     for (int nch = 1; nch <= nxs; ++nch) {
