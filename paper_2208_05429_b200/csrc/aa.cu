@@ -19,8 +19,11 @@
 //
 // The collision is bgk_collide() and the wall/lid rules are those of
 // pull_cell() (R-4..R-7), so AA steps reproduce K1
-// steps bit for bit (tests/test_gpu_parity.py).  One process, one slab:
-// x-periodicity wraps in the kernel.
+// steps bit for bit (tests/test_gpu_parity.py).  A single slab wraps x in
+// the kernel; X-slabs use the ghost planes x = -1 and nx_local, filled
+// before every odd step (the neighbours' c_x = -1 / +1 slots of their edge
+// planes) and returned after it (what the odd step scattered into them
+// belongs to the neighbours' edge cells): api.cu exchange_aa().
 #include "kernels.h"
 
 namespace lbm {
@@ -36,16 +39,19 @@ __device__ __forceinline__ long long aa_nbr(const SlabGeom& g, int x, int y, int
     int nx_ = x + dx, ny_ = y + dy, nz_ = z + dz;
     if constexpr (BC == BC_CAVITY) {
         bool out = false;
-        if constexpr (dx == -1) out = out || x == 0;
-        if constexpr (dx == 1) out = out || x == g.nxl - 1;
+        // x: a wall only at the slab ends that are domain walls; otherwise
+        // the neighbour lies in a ghost plane (x = -1 or nxl)
+        if constexpr (dx == -1) out = out || (x == 0 && g.left_wall);
+        if constexpr (dx == 1) out = out || (x == g.nxl - 1 && g.right_wall);
         if constexpr (dy == -1) out = out || y == 0;
         if constexpr (dy == 1) out = out || y == g.ny - 1;
         if constexpr (dz == -1) out = out || z == 0;
         if constexpr (dz == 1) out = out || z == g.nz - 1;
         if (out) return -1;
     } else {
-        if constexpr (dx == -1) nx_ = x == 0 ? g.nxl - 1 : nx_;
-        if constexpr (dx == 1) nx_ = x == g.nxl - 1 ? 0 : nx_;
+        // x wraps in the kernel only for a single slab; slabs use ghost planes
+        if constexpr (dx == -1) nx_ = (x == 0 && g.nxl == g.nx) ? g.nxl - 1 : nx_;
+        if constexpr (dx == 1) nx_ = (x == g.nxl - 1 && g.nxl == g.nx) ? 0 : nx_;
         if constexpr (dy == -1) ny_ = y == 0 ? g.ny - 1 : ny_;
         if constexpr (dy == 1) ny_ = y == g.ny - 1 ? 0 : ny_;
         if constexpr (dz == -1) nz_ = z == 0 ? g.nz - 1 : nz_;
@@ -173,11 +179,39 @@ __global__ void __launch_bounds__(256) k_aa_moments(const T* __restrict__ F, Ste
     }
 }
 
+// Reverse AA halo: copy the five slot-planes [slot0, slot0 + 5) of a ghost
+// plane (src) into the owner's edge plane (dst), only the entries the odd
+// step actually scattered there -- those whose writer (y - c_y, z - c_z) is
+// a cell (periodic: all).  In a cavity the rim entries were written by the
+// owner itself (its wall rule) and must not be overwritten with the stale
+// forward copy.
+template <typename T>
+__global__ void __launch_bounds__(256) k_aa_merge(T* __restrict__ dst, const T* __restrict__ src, SlabGeom g,
+                                                 int slot0) {
+    const int z = blockIdx.x * 32 + threadIdx.x;
+    const int y = blockIdx.y * 8 + threadIdx.y;
+    const int m = blockIdx.z;  // 0..4
+    if (z >= g.nz || y >= g.ny) return;
+    const int k = slot0 + m;
+    const int i = slot_dir(k);
+    const int sy = y - can_cy(i), sz = z - can_cz(i);
+    // periodic: every entry has a (wrapped) writer
+    if (g.bc == BC_CAVITY && (sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz)) return;
+    const long long o = (long long)m * g.pq + (long long)y * g.nzp + z;
+    dst[o] = src[o];
+}
+
 // ------------------------------------------------------------ launchers --
 namespace {
 dim3 aa_grid(int nz, int ny, int nx) { return dim3((nz + 31) / 32, (ny + 7) / 8, nx); }
 const dim3 kAABlock(32, 8, 1);
 }  // namespace
+
+template <typename T>
+cudaError_t launch_aa_merge(T* dst, const T* src, const SlabGeom& g, int slot0, cudaStream_t s) {
+    k_aa_merge<T><<<aa_grid(g.nz, g.ny, 5), kAABlock, 0, s>>>(dst, src, g, slot0);
+    return cudaGetLastError();
+}
 
 template <typename T>
 cudaError_t launch_aa_step(T* F, const StepParams<T>& P, bool odd, cudaStream_t s) {
@@ -220,7 +254,8 @@ cudaError_t launch_aa_moments(const T* F, const StepParams<T>& P, bool odd, int 
     template cudaError_t launch_aa_materialize<T>(const T*, const StepParams<T>&, bool, int, int, int, int,   \
                                                   int, int, double*, cudaStream_t);                          \
     template cudaError_t launch_aa_moments<T>(const T*, const StepParams<T>&, bool, int, int, double*,       \
-                                              double*, cudaStream_t);
+                                              double*, cudaStream_t);                                        \
+    template cudaError_t launch_aa_merge<T>(T*, const T*, const SlabGeom&, int, cudaStream_t);
 LBM_AA_INSTANTIATE(double)
 LBM_AA_INSTANTIATE(float)
 

@@ -230,6 +230,87 @@ lbm_status exchange(lbm_ctx* c, int which, cudaStream_t st) {
     return LBM_OK;
 }
 
+// AA X-slab halo (aa.cu).  forward (before an odd step or an odd-phase
+// read-back): ghost x = -1 <- left's plane nxl-1, c_x = -1 slots; ghost
+// x = nxl <- right's plane 0, c_x = +1 slots.  reverse (after an odd step):
+// those ghost slots, now holding what the odd step scattered into the
+// neighbours' edge cells, go back to the same neighbour locations.
+// Five slot-planes per side, one contiguous run each.
+template <typename T>
+lbm_status exchange_aa_t(lbm_ctx* c, bool forward) {
+    const size_t es = sizeof(T);
+    auto off = [](const Slab& s, int x, int slot0) {
+        return ((long long)(x + 2) * s.plan.plane_x + (long long)slot0 * s.plan.plane_q);
+    };
+    if (c->opts.comm == LBM_COMM_NCCL) {
+        Slab& s = c->slabs[0];
+        T* b = static_cast<T*>(s.buf[0]);
+        const ncclDataType_t ty = c->dt == LBM_F64 ? ncclFloat64 : ncclFloat32;
+        const size_t n = size_t(5 * s.plan.plane_q);
+        const int nxl = s.g.nxl;
+        // reverse: received into scratch (the staging buffer), then merged
+        T* scratch_r = static_cast<T*>(c->stage);  // from right -> my (nxl-1, M)
+        T* scratch_l = scratch_r + n;               // from left  -> my (0, P)
+        if (!forward && 2 * n * es > c->stage_bytes) return fail(c, LBM_ENOMEM, "AA halo scratch too small");
+        CKN(g_nccl.GroupStart());
+        if (forward) {
+            // to left: my (0, P) -> its ghost (nxl, P); to right: my (nxl-1, M) -> its ghost (-1, M)
+            if (s.left >= 0) CKN(g_nccl.Send(b + off(s, 0, kSlotP0), n, ty, s.left, c->comm, c->stream));
+            if (s.right >= 0) CKN(g_nccl.Recv(b + off(s, nxl, kSlotP0), n, ty, s.right, c->comm, c->stream));
+            if (s.right >= 0) CKN(g_nccl.Send(b + off(s, nxl - 1, 0), n, ty, s.right, c->comm, c->stream));
+            if (s.left >= 0) CKN(g_nccl.Recv(b + off(s, -1, 0), n, ty, s.left, c->comm, c->stream));
+        } else {
+            // to left: my ghost (-1, M) -> its (nxl-1, M); to right: my ghost (nxl, P) -> its (0, P)
+            if (s.left >= 0) CKN(g_nccl.Send(b + off(s, -1, 0), n, ty, s.left, c->comm, c->stream));
+            if (s.right >= 0) CKN(g_nccl.Recv(scratch_r, n, ty, s.right, c->comm, c->stream));
+            if (s.right >= 0) CKN(g_nccl.Send(b + off(s, nxl, kSlotP0), n, ty, s.right, c->comm, c->stream));
+            if (s.left >= 0) CKN(g_nccl.Recv(scratch_l, n, ty, s.left, c->comm, c->stream));
+        }
+        CKN(g_nccl.GroupEnd());
+        if (!forward) {
+            if (s.right >= 0) CK(launch_aa_merge<T>(b + off(s, nxl - 1, 0), scratch_r, s.g, 0, c->stream));
+            if (s.left >= 0) CK(launch_aa_merge<T>(b + off(s, 0, kSlotP0), scratch_l, s.g, kSlotP0, c->stream));
+        }
+        return LBM_OK;
+    }
+    for (Slab& s : c->slabs) {
+        const size_t bytes = size_t(5 * s.plan.plane_q) * es;
+        T* mine = static_cast<T*>(s.buf[0]);
+        if (s.left >= 0) {
+            Slab& L = c->slabs[s.left];
+            T* theirs = static_cast<T*>(L.buf[0]);
+            if (forward)
+                CK(cudaMemcpyAsync(mine + off(s, -1, 0), theirs + off(L, L.g.nxl - 1, 0), bytes,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+            else
+                CK(launch_aa_merge<T>(theirs + off(L, L.g.nxl - 1, 0), mine + off(s, -1, 0), s.g, 0, c->stream));
+        }
+        if (s.right >= 0) {
+            Slab& R = c->slabs[s.right];
+            T* theirs = static_cast<T*>(R.buf[0]);
+            if (forward)
+                CK(cudaMemcpyAsync(mine + off(s, s.g.nxl, kSlotP0), theirs + off(R, 0, kSlotP0), bytes,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+            else
+                CK(launch_aa_merge<T>(theirs + off(R, 0, kSlotP0), mine + off(s, s.g.nxl, kSlotP0), s.g, kSlotP0,
+                                      c->stream));
+        }
+    }
+    return LBM_OK;
+}
+
+lbm_status exchange_aa(lbm_ctx* c, bool forward) {
+    return c->dt == LBM_F64 ? exchange_aa_t<double>(c, forward) : exchange_aa_t<float>(c, forward);
+}
+
+bool aa_has_halo(const lbm_ctx* c) {
+    // a single slab wraps x in the kernel; otherwise slabs with neighbours exchange
+    if (c->slabs.size() == 1 && c->opts.world == 1) return false;
+    for (const Slab& s : c->slabs)
+        if (s.left >= 0 || s.right >= 0) return true;
+    return false;
+}
+
 bool has_neighbours(const lbm_ctx* c) {
     for (const Slab& s : c->slabs)
         if (s.left >= 0 || s.right >= 0) return true;
@@ -237,7 +318,15 @@ bool has_neighbours(const lbm_ctx* c) {
 }
 
 lbm_status ensure_ghosts(lbm_ctx* c) {
-    if (c->ghosts_valid || !has_neighbours(c) || c->aa) {  // AA wraps x in the kernels
+    if (c->aa) {  // odd phase: the gather reads the neighbours' edge slots
+        if (c->aa_odd && !c->ghosts_valid && aa_has_halo(c)) {
+            lbm_status st = exchange_aa(c, true);
+            if (st != LBM_OK) return st;
+        }
+        c->ghosts_valid = true;
+        return LBM_OK;
+    }
+    if (c->ghosts_valid || !has_neighbours(c)) {
         c->ghosts_valid = true;
         return LBM_OK;
     }
@@ -282,19 +371,31 @@ lbm_status prof_end(lbm_ctx* c, size_t slot, long long updates) {
 // single-copy AA storage: alternate the in-place even / odd steps (aa.cu)
 template <typename T>
 lbm_status run_steps_aa(lbm_ctx* c, long n) {
-    Slab& s = c->slabs[0];
-    const StepParams<T> P = make_params<T>(c, s);
+    const bool halo = aa_has_halo(c);
     for (; n > 0; --n) {
         size_t slot = 0;
+        long long updates = 0;
         lbm_status st = prof_begin(c, slot);
         if (st != LBM_OK) return st;
-        cudaError_t e = launch_aa_step<T>(static_cast<T*>(s.buf[0]), P, c->aa_odd, c->stream);
-        if (e != cudaSuccess) return fail(c, LBM_ECUDA, "AA step launch failed: %s", cudaGetErrorString(e));
-        c->launches++;
-        c->k1_launches++;
-        st = prof_end(c, slot, (long long)s.g.nxl * s.g.ny * s.g.nz);
+        if (c->aa_odd && halo && !c->ghosts_valid) {
+            st = exchange_aa(c, true);
+            if (st != LBM_OK) return st;
+        }
+        for (Slab& s : c->slabs) {
+            cudaError_t e = launch_aa_step<T>(static_cast<T*>(s.buf[0]), make_params<T>(c, s), c->aa_odd, c->stream);
+            if (e != cudaSuccess) return fail(c, LBM_ECUDA, "AA step launch failed: %s", cudaGetErrorString(e));
+            c->launches++;
+            c->k1_launches++;
+            updates += (long long)s.g.nxl * s.g.ny * s.g.nz;
+        }
+        if (c->aa_odd && halo) {
+            st = exchange_aa(c, false);
+            if (st != LBM_OK) return st;
+        }
+        st = prof_end(c, slot, updates);
         if (st != LBM_OK) return st;
         c->aa_odd = !c->aa_odd;
+        c->ghosts_valid = false;
         c->t += 1;
     }
     return LBM_OK;
@@ -402,6 +503,7 @@ lbm_status finish_init(lbm_ctx* c, int canon) {
     if (c->aa) {  // canonical f(t0) in buf[0] IS the at-rest AA state
         c->cur = 0;
         c->aa_odd = false;
+        c->ghosts_valid = false;
         c->initialized = true;
         c->t = 0;
         return LBM_OK;
@@ -427,39 +529,41 @@ lbm_status finish_init(lbm_ctx* c, int canon) {
 template <typename T>
 lbm_status init_eq_aa(lbm_ctx* c, const double* rho, const double* u, bool host) {
     const long long plane = (long long)c->ny * c->nz;
-    Slab& s = c->slabs[0];
-    T* F = static_cast<T*>(s.buf[0]);
-    if (!host) {
-        CK(launch_k0_equilibrium<T>(rho, u, F, s.g, c->stream));
-        c->launches++;
-        return finish_init<T>(c, 0);
-    }
     // planes per chunk: 32 B (rho + u) per cell in the staging buffer
     const int cap = int(std::max<long long>(1, (long long)(c->stage_bytes / (4 * sizeof(double))) / plane));
     double* stage = static_cast<double*>(c->stage);
-    for (int xb = 0; xb < s.g.nxl; xb += cap) {
-        const int nxc = std::min(cap, s.g.nxl - xb);
-        const long long cells = (long long)nxc * plane;
-        const double* dr = nullptr;
-        const double* du = nullptr;
-        if (rho) {
-            CK(cudaMemcpyAsync(stage, rho + (long long)xb * plane, cells * sizeof(double), cudaMemcpyHostToDevice,
-                               c->stream));
-            dr = stage;
+    for (Slab& s : c->slabs) {
+        T* F = static_cast<T*>(s.buf[0]);
+        const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;  // process-local cell offset
+        if (!host) {
+            CK(launch_k0_equilibrium<T>(rho ? rho + xoff : nullptr, u ? u + 3 * xoff : nullptr, F, s.g, c->stream));
+            c->launches++;
+            continue;
         }
-        if (u) {
-            CK(cudaMemcpyAsync(stage + cells, u + 3 * (long long)xb * plane, 3 * cells * sizeof(double),
-                               cudaMemcpyHostToDevice, c->stream));
-            du = stage + cells;
+        for (int xb = 0; xb < s.g.nxl; xb += cap) {
+            const int nxc = std::min(cap, s.g.nxl - xb);
+            const long long cells = (long long)nxc * plane;
+            const long long hoff = xoff + (long long)xb * plane;
+            const double* dr = nullptr;
+            const double* du = nullptr;
+            if (rho) {
+                CK(cudaMemcpyAsync(stage, rho + hoff, cells * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+                dr = stage;
+            }
+            if (u) {
+                CK(cudaMemcpyAsync(stage + cells, u + 3 * hoff, 3 * cells * sizeof(double), cudaMemcpyHostToDevice,
+                                   c->stream));
+                du = stage + cells;
+            }
+            int flag = 0;
+            lbm_status st;
+            if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
+            if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+            if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
+            if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+            CK(launch_k0_equilibrium<T>(dr, du, F, s.g, c->stream, xb, nxc));
+            c->launches++;
         }
-        int flag = 0;
-        lbm_status st;
-        if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
-        if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
-        if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
-        if (flag) return fail(c, LBM_EINVAL, "u must be finite");
-        CK(launch_k0_equilibrium<T>(dr, du, F, s.g, c->stream, xb, nxc));
-        c->launches++;
     }
     return finish_init<T>(c, 0);
 }
@@ -533,31 +637,36 @@ lbm_status set_pops(lbm_ctx* c, const double* f) {
 
 template <typename T>
 lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
+    lbm_status st = ensure_ghosts(c);
+    if (st != LBM_OK) return st;
     const long long plane = (long long)c->ny * c->nz;
-    Slab& s = c->slabs[0];
-    const StepParams<T> P = make_params<T>(c, s);
-    const T* F = static_cast<const T*>(s.buf[0]);
-    if (!host) {
-        CK(launch_aa_moments<T>(F, P, c->aa_odd, 0, s.g.nxl, rho, u, c->stream));
-        c->launches++;
-        return LBM_OK;
-    }
     const int cap = int(std::max<long long>(1, (long long)(c->stage_bytes / (4 * sizeof(double))) / plane));
     double* stage = static_cast<double*>(c->stage);
-    for (int xb = 0; xb < s.g.nxl; xb += cap) {
-        const int nxc = std::min(cap, s.g.nxl - xb);
-        const long long cells = (long long)nxc * plane;
-        CK(launch_aa_moments<T>(F, P, c->aa_odd, xb, nxc, rho ? stage : nullptr, u ? stage + cells : nullptr,
-                                c->stream));
-        c->launches++;
-        if (rho)
-            CK(cudaMemcpyAsync(rho + (long long)xb * plane, stage, cells * sizeof(double), cudaMemcpyDeviceToHost,
-                               c->stream));
-        if (u)
-            CK(cudaMemcpyAsync(u + 3 * (long long)xb * plane, stage + cells, 3 * cells * sizeof(double),
-                               cudaMemcpyDeviceToHost, c->stream));
+    for (Slab& s : c->slabs) {
+        const StepParams<T> P = make_params<T>(c, s);
+        const T* F = static_cast<const T*>(s.buf[0]);
+        const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;
+        if (!host) {
+            CK(launch_aa_moments<T>(F, P, c->aa_odd, 0, s.g.nxl, rho ? rho + xoff : nullptr,
+                                    u ? u + 3 * xoff : nullptr, c->stream));
+            c->launches++;
+            continue;
+        }
+        for (int xb = 0; xb < s.g.nxl; xb += cap) {
+            const int nxc = std::min(cap, s.g.nxl - xb);
+            const long long cells = (long long)nxc * plane;
+            const long long hoff = xoff + (long long)xb * plane;
+            CK(launch_aa_moments<T>(F, P, c->aa_odd, xb, nxc, rho ? stage : nullptr, u ? stage + cells : nullptr,
+                                    c->stream));
+            c->launches++;
+            if (rho)
+                CK(cudaMemcpyAsync(rho + hoff, stage, cells * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            if (u)
+                CK(cudaMemcpyAsync(u + 3 * hoff, stage + cells, 3 * cells * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        }
     }
-    CK(cudaStreamSynchronize(c->stream));
+    if (host) CK(cudaStreamSynchronize(c->stream));
     return LBM_OK;
 }
 
@@ -701,8 +810,9 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     if (o.comm == LBM_COMM_LOCAL && o.world != 1) return fail(c, LBM_EINVAL, "comm LOCAL needs world == 1");
     if (o.comm < LBM_COMM_NONE || o.comm > LBM_COMM_LOCAL) return fail(c, LBM_EINVAL, "bad comm %d", o.comm);
     if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_AA) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
-    if (o.kernel == LBM_KERNEL_AA && (o.world != 1 || o.local_slabs != 1))
-        return fail(c, LBM_EINVAL, "kernel AA (single-copy storage) needs world == 1 and local_slabs == 1");
+    if (o.kernel == LBM_KERNEL_AA && o.bc == LBM_BC_CAVITY && (o.world > 1 || o.local_slabs > 1) &&
+        nx / (o.world * o.local_slabs) < 2)
+        return fail(c, LBM_EINVAL, "kernel AA with X-slabs needs >= 2 planes per slab");
     const int nslab_total = o.world * o.local_slabs;
     if (nx % nslab_total) return fail(c, LBM_EINVAL, "nx %d not divisible by %d slabs", nx, nslab_total);
     const int nxl = nx / nslab_total;

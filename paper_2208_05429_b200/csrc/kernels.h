@@ -37,6 +37,8 @@ template <typename T>
 cudaError_t launch_aa_materialize(const T* F, const StepParams<T>& P, bool odd, int x0, int y0, int z0, int lx,
                                   int ly, int lz, double* out, cudaStream_t s);
 template <typename T>
+cudaError_t launch_aa_merge(T* dst, const T* src, const SlabGeom& g, int slot0, cudaStream_t s);
+template <typename T>
 cudaError_t launch_aa_moments(const T* F, const StepParams<T>& P, bool odd, int xbeg, int nxc, double* rho,
                               double* u, cudaStream_t s);
 template <typename T>

@@ -352,8 +352,33 @@ def test_aa_config2_init_equilibrium_and_errors():
         lbm.lbm_init_equilibrium_device(lat.ctx, rd, ud)
         lat.step(30)
         assert np.array_equal(lat.populations(), outs[1][0])
-    with pytest.raises(lbm.LbmError):
-        lbm.Lattice(16, 8, 8, 0.6, LID, "f64", kernel=lbm.LBM_KERNEL_AA, comm=lbm.LBM_COMM_LOCAL, local_slabs=2)
+    with pytest.raises(lbm.LbmError):  # cavity slabs of one plane
+        lbm.Lattice(4, 8, 8, 0.6, LID, "f64", kernel=lbm.LBM_KERNEL_AA, comm=lbm.LBM_COMM_LOCAL, local_slabs=4)
+
+
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
+@pytest.mark.parametrize("slabs", [2, 4])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_aa_local_slabs_bitwise(bc, slabs, dtype):
+    """AA over X-slabs (LOCAL transport on one device): the forward halo
+    before each odd step and the reverse halo after it give the single-slab
+    AA bits after every step count, including odd-phase read-backs."""
+    dims = (16, 12, 20)
+    f0 = li.random_populations(59, *dims)
+    runs = []
+    for s_ in (1, slabs):
+        kw = dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=s_) if s_ > 1 else {}
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=bc, kernel=lbm.LBM_KERNEL_AA, **kw) as lat:
+            lat.set_populations(f0)
+            out = []
+            for n in (1, 2, 1, 3):
+                lat.step(n)
+                out.append((lat.populations(), *lat.macroscopic()))
+            runs.append(out)
+    for a, b in zip(*runs):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    assert relerr_floor(runs[1][-1][0], oracle.run(f0, bc, 0.6, LID, 7)) <= TOL[dtype]
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
