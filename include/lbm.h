@@ -91,8 +91,10 @@ typedef enum {
      * the paper's one-lattice swap): one lattice
      * buffer instead of two (half the memory), alternating an in-place
      * collide-and-revert step with a gather/scatter step; one step per HBM
-     * pass (K1's bytes).  Needs world == 1 and local_slabs == 1 (EINVAL
-     * otherwise).  Bitwise identical to K1. */
+     * pass (K1's bytes).  X-slabs exchange five slot-planes per side before
+     * and after each odd step; cavity slabs need >= 2 planes (EINVAL).
+     * Bitwise identical to K1 without a lid (with it, K1's pull storage
+     * rounds the lid term once more: agreement to ~1 ulp). */
     LBM_KERNEL_AA = 4
 } lbm_kernel;
 
