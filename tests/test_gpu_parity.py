@@ -454,3 +454,39 @@ def test_full_size_sampled_parity(cfg_id, dtype):
             known = ~np.isnan(r)
             assert known.sum() > 0.15 * r.size
             assert relerr(g[known], r[known]) <= TOL[dtype], (cfg.name, o)
+
+
+def test_randomised_configurations_bitwise():
+    """Property check over random small lattices (seeded): for any dims,
+    boundary mode, dtype, kernel (K2, K2_REG, AA), slab count and split of
+    the step count, the result equals K1 on one slab bit for bit (AA: no
+    lid, see test_aa_single_copy_equals_k1), and K1 matches the oracle."""
+    rng = np.random.default_rng(2208)
+    for trial in range(24):
+        bc = int(rng.integers(0, 2))
+        slabs = int(rng.choice([1, 1, 2, 3]))
+        nxl = int(rng.integers(2 if slabs == 1 else 4, 9))
+        dims = (nxl * slabs, int(rng.integers(1, 19)), int(rng.integers(1, 45)))
+        if bc == lbm.LBM_BC_PERIODIC and dims[0] < 2:
+            continue
+        dtype = str(rng.choice(["f64", "f32"]))
+        kernel = int(rng.choice([lbm.LBM_KERNEL_K2, lbm.LBM_KERNEL_K2_REG, lbm.LBM_KERNEL_AA]))
+        lid = (0.0, 0.0, 0.0) if kernel == lbm.LBM_KERNEL_AA else (float(rng.uniform(-0.05, 0.05)),
+                                                                    float(rng.uniform(-0.05, 0.05)), 0.0)
+        splits = [int(v) for v in rng.integers(0, 4, size=int(rng.integers(1, 4)))]
+        tau = float(rng.uniform(0.52, 1.5))
+        f0 = li.random_populations(100 + trial, *dims)
+        with lbm.Lattice(*dims, tau, lid, dtype, bc=bc, kernel=lbm.LBM_KERNEL_K1) as ref:
+            ref.set_populations(f0)
+            ref.step(sum(splits))
+            want = ref.populations()
+        kw = dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=slabs) if slabs > 1 else {}
+        with lbm.Lattice(*dims, tau, lid, dtype, bc=bc, kernel=kernel, **kw) as lat:
+            lat.set_populations(f0)
+            for n in splits:
+                lat.step(n)
+            got = lat.populations()
+        case = (dims, bc, dtype, kernel, slabs, splits, tau)
+        assert np.array_equal(got, want), case
+        if dtype == "f64":
+            assert relerr_floor(want, oracle.run(f0, bc, tau, lid, sum(splits))) <= 1e-12, case
