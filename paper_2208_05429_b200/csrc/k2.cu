@@ -64,7 +64,11 @@ struct K2Cfg {
     // ring depth per group (destination planes live at once, see the loop)
     static constexpr int NM = 2, NZ = 3, NP = 4;
     static constexpr int RING = (NM * 5 + NZ * 9 + NP * 5) * RP;  // 57 direction-planes
-    static constexpr size_t SMEM = size_t(2 * kQ * BOXE + RING) * sizeof(T) + 2 * sizeof(uint64_t);
+    // cavity wall-link values of the next plane, prefetched per thread with
+    // cp.async: [2 buffers][HZ wall-row lanes + HY wall-column lanes][5 slots]
+    static constexpr int WALLE = (HZ + HY) * 5;
+    static constexpr size_t SMEM =
+        size_t(2 * kQ * BOXE + RING + 2 * WALLE) * sizeof(T) + 2 * sizeof(uint64_t);
     static constexpr uint32_t TX_BYTES = uint32_t(kQ * BOX * sizeof(T));
     // CTAs per SM: what shared memory (228 KB per SM, 1 KB reserved per CTA)
     // and registers (about 168 per thread in fp64, 96 in fp32) allow
@@ -74,6 +78,27 @@ struct K2Cfg {
     static constexpr int MINB_RAW = BY_SMEM < BY_REGS ? BY_SMEM : BY_REGS;
     static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 3 ? 3 : MINB_RAW);
 };
+
+// position of slot k among the slots whose c_y (dim 1) / c_z (dim 2) equals sgn
+__host__ __device__ constexpr int wall_idx(int k, int dim, int sgn) {
+    int m = 0;
+    for (int j = 0; j < k; ++j) {
+        const int i = slot_dir(j);
+        if ((dim == 1 ? can_cy(i) : can_cz(i)) == sgn) ++m;
+    }
+    return m;
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -129,7 +154,8 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     T* const ringM = stage + 2 * kQ * C::BOXE;
     T* const ringZ = ringM + C::NM * 5 * C::RP;
     T* const ringP = ringZ + C::NZ * 9 * C::RP;
-    uint64_t* const bar = reinterpret_cast<uint64_t*>(ringP + C::NP * 5 * C::RP);
+    T* const wallbuf = ringP + C::NP * 5 * C::RP;  // [2][HZ + HY][5]
+    uint64_t* const bar = reinterpret_cast<uint64_t*>(wallbuf + 2 * C::WALLE);
 
     const SlabGeom& g = P.g;
     const int ntz = (g.nz + TZ - 1) / TZ;
@@ -199,6 +225,47 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool rowok[3] = {a >= 2 && a <= TY + 1, a >= 1 && a <= TY, a <= TY - 1};
     const bool colok[3] = {b >= 2 && b <= TZ + 1, b >= 1 && b <= TZ, b <= TZ - 1};
     const bool edge_tile = BC == BC_CAVITY && (edge_y || edge_z);
+    // Cavity wall lanes of this tile: the box row holding y = 0 or y = ny-1
+    // and the box column holding z = 0 or z = nz-1 (at most one of each;
+    // otherwise -- tiny domains -- the direct loads below).  Their wall-link
+    // values (the cell's own opposite slots) are prefetched one plane ahead
+    // into shared memory with cp.async, off the critical path.
+    int wrow = -1, wcol = -1, wsy = 0, wsz = 0;  // wsy / wsz: c_y / c_z of the wall slots
+    bool wb_ok = false;
+    if constexpr (BC == BC_CAVITY) {
+        const int r0 = y0 <= 1 ? 1 - y0 : -1, r1 = (g.ny - y0 >= 0 && g.ny - y0 <= C::HY - 1) ? g.ny - y0 : -1;
+        const int c0 = z0 <= 1 ? 1 - z0 : -1, c1 = (g.nz - z0 >= 0 && g.nz - z0 <= C::HZ - 1) ? g.nz - z0 : -1;
+        wb_ok = edge_tile && !(r0 >= 0 && r1 >= 0) && !(c0 >= 0 && c1 >= 0);
+        if (r0 >= 0) { wrow = r0; wsy = 1; } else if (r1 >= 0) { wrow = r1; wsy = -1; }
+        if (c0 >= 0) { wcol = c0; wsz = 1; } else if (c1 >= 0) { wcol = c1; wsz = -1; }
+    }
+    const bool wl_row = wb_ok && q_in && a == wrow, wl_col = wb_ok && q_in && b == wcol;
+    auto wall_prefetch = [&](int pn, int buf) {  // this thread's wall values of plane pn
+        if (!(wl_row || wl_col)) return;
+        const T* const selfp = A + cell_off(g, pn, qy, qz);
+        T* const wb = wallbuf + buf * C::WALLE;
+        static_for<0, kQ>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            constexpr int i = slot_dir(k);
+            constexpr int cy = can_cy(i), cz = can_cz(i);
+            if constexpr (cy != 0) {
+                if (wl_row && cy == wsy) {
+                    T* d = wb + b * 5 + wall_idx(k, 1, cy);
+                    if constexpr (sizeof(T) == 8) cp_async8(d, selfp + (long long)slot_opp(k) * g.pq);
+                    else cp_async4(d, selfp + (long long)slot_opp(k) * g.pq);
+                }
+            }
+            if constexpr (cz != 0) {
+                if (wl_col && cz == wsz) {
+                    T* d = wb + (C::HZ + a) * 5 + wall_idx(k, 2, cz);
+                    if constexpr (sizeof(T) == 8) cp_async8(d, selfp + (long long)slot_opp(k) * g.pq);
+                    else cp_async4(d, selfp + (long long)slot_opp(k) * g.pq);
+                }
+            }
+        });
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (p_first <= p_last) wall_prefetch(p_first, 0);
 
     // Software pipeline, ONE block barrier per plane (after the stage read).
     // Iteration p runs, in the same phase, step 2 of destination plane p-2
@@ -255,7 +322,41 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                     // the staged entry (TMA zero fill, or a cell beyond the x
                     // wall) is replaced by the cell's own opposite population
                     // (+ lid), per thread -- the arithmetic of pull_cell().
-                    if ((edge_tile || lwall || rwall) && q_in) {
+                    if (wb_ok && !lwall && !rwall) {
+                        // prefetched wall values of this plane (buffer c & 1),
+                        // then the next plane's prefetch into the other buffer
+                        if (wl_row || wl_col) {
+                            asm volatile("cp.async.wait_group 0;" ::: "memory");
+                            const T* const wb = wallbuf + (c & 1) * C::WALLE;
+                            static_for<0, kQ>([&](auto kc) {
+                                constexpr int k = decltype(kc)::value;
+                                constexpr int i = slot_dir(k);
+                                constexpr int cy = can_cy(i), cz = can_cz(i);
+                                bool hit = false;
+                                T v = T(0);
+                                if constexpr (cy != 0) {
+                                    if (wl_row && cy == wsy) {
+                                        v = wb[b * 5 + wall_idx(k, 1, cy)];
+                                        hit = true;
+                                    }
+                                }
+                                if constexpr (cz != 0) {
+                                    if (wl_col && cz == wsz) {
+                                        v = wb[(C::HZ + a) * 5 + wall_idx(k, 2, cz)];
+                                        hit = true;
+                                    }
+                                }
+                                if (hit) {
+                                    if constexpr (cz == -1) {
+                                        if (qz == g.nz - 1) v = v + P.lid[k];
+                                    }
+                                    fs[i] = v;
+                                }
+                            });
+                        }
+                        if (p + 1 <= p_last) wall_prefetch(p + 1, (c + 1) & 1);
+                    } else if ((edge_tile || lwall || rwall) && q_in) {
+                        if (wb_ok && p + 1 <= p_last) wall_prefetch(p + 1, (c + 1) & 1);
                         const long long self = cell_off(g, p, qy, qz);
                         static_for<0, kQ>([&](auto kc) {
                             constexpr int k = decltype(kc)::value;
