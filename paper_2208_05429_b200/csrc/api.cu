@@ -600,6 +600,17 @@ lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
             dr = rho ? rho + xoff : nullptr;
             du = u ? u + 3 * xoff : nullptr;
         }
+        if (c->slabs.size() == 1 && c->opts.world == 1) {
+            // one slab spanning the domain: the pull-form state in one pass
+            // (k0_init_pull), the staging (host inputs) in the other buffer
+            CK(launch_k0_init_pull<T>(dr, du, static_cast<T*>(s.buf[canon]), make_params<T>(c, s), c->stream));
+            c->launches++;
+            c->cur = canon;
+            c->ghosts_valid = false;
+            c->initialized = true;
+            c->t = 0;
+            return LBM_OK;
+        }
         CK(launch_k0_equilibrium<T>(dr, du, static_cast<T*>(s.buf[canon]), s.g, c->stream));
         c->launches++;
     }

@@ -105,6 +105,102 @@ __global__ void __launch_bounds__(256) k0_unstream(const T* __restrict__ C, T* _
     });
 }
 
+// K0 fused (one slab holding the whole x range): the pull-form initial state
+// S^-1(feq(rho, u)) in one pass, without the canonical intermediate.  Slot k
+// (direction j) of cell y takes feq_j of the cell y + c_j (x, y, z wrapped
+// when periodic), or, through a cavity wall, feq_opp(j)(y) - lid_opp; feq_j
+// of a neighbour is the single-direction form of eq_pairs() -- the same
+// operations, so the same bits as k0_equilibrium + k0_unstream.
+template <typename T>
+__device__ __forceinline__ void k0_load(const double* rho, const double* u, long long cell, T& r, T& ux, T& uy,
+                                        T& uz) {
+    r = rho ? T(rho[cell]) : T(1);
+    ux = uy = uz = T(0);
+    if (u) {
+        ux = T(u[3 * cell + 0]);
+        uy = T(u[3 * cell + 1]);
+        uz = T(u[3 * cell + 2]);
+    }
+}
+
+template <typename T, int j>
+__device__ __forceinline__ T feq_dir(T W, T ux, T uy, T uz) {
+    // the per-pair arithmetic of eq_pairs<T, false> for direction j (1..18)
+    constexpr int i = j <= 9 ? j : j - 9;  // pair representative
+    constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
+    const T usq = fma(ux, ux, fma(uy, uy, uz * uz));
+    const T base = fma(T(-1.5), usq, T(1));
+    const T Wa = W * T(1.0 / 18.0);
+    const T Aa = Wa * base, Ba = T(4.5) * Wa, Ca = T(3) * Wa;
+    const T Ad = T(0.5) * Aa, Bd = T(0.5) * Ba, Cd = T(0.5) * Ca;
+    T cu;
+    if constexpr (cx != 0 && cy != 0) cu = (cx > 0 ? ux : -ux) + (cy > 0 ? uy : -uy);
+    else if constexpr (cx != 0 && cz != 0) cu = (cx > 0 ? ux : -ux) + (cz > 0 ? uz : -uz);
+    else if constexpr (cy != 0 && cz != 0) cu = (cy > 0 ? uy : -uy) + (cz > 0 ? uz : -uz);
+    else if constexpr (cx != 0) cu = cx > 0 ? ux : -ux;
+    else if constexpr (cy != 0) cu = cy > 0 ? uy : -uy;
+    else cu = cz > 0 ? uz : -uz;
+    constexpr bool ax = can_axis(i);
+    const T common = fma((ax ? Ba : Bd) * cu, cu, ax ? Aa : Ad);
+    const T C = ax ? Ca : Cd;
+    return j <= 9 ? fma(C, cu, common) : fma(-C, cu, common);
+}
+
+template <typename T, int BC>
+__global__ void __launch_bounds__(256) k0_init_pull(const double* __restrict__ rho, const double* __restrict__ u,
+                                                   T* __restrict__ A, StepParams<T> P) {
+    const int z = blockIdx.x * 32 + threadIdx.x;
+    const int y = blockIdx.y * 8 + threadIdx.y;
+    const int x = blockIdx.z;
+    const SlabGeom& g = P.g;
+    if (z >= g.nz || y >= g.ny) return;
+    auto cell_of = [&](int xx, int yy, int zz) { return ((long long)xx * g.ny + yy) * g.nz + zz; };
+    T r, ux, uy, uz;
+    k0_load<T>(rho, u, cell_of(x, y, z), r, ux, uy, uz);
+    T feq[kQ];
+    equilibrium<T>(r, ux, uy, uz, feq);  // own cell: slot 0 and the wall links
+    const long long self = cell_off(g, x, y, z);
+    static_for<0, kQ>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        constexpr int j = slot_dir(k);
+        constexpr int cx = can_cx(j), cy = can_cy(j), cz = can_cz(j);
+        T v;
+        if constexpr (j == 0) {
+            v = feq[0];
+        } else {
+            int tx = x + cx, ty = y + cy, tz = z + cz;
+            bool wall = false;
+            if constexpr (BC == BC_CAVITY) {
+                if constexpr (cx == -1) wall = wall || x == 0;
+                if constexpr (cx == 1) wall = wall || x == g.nxl - 1;
+                if constexpr (cy == -1) wall = wall || y == 0;
+                if constexpr (cy == 1) wall = wall || y == g.ny - 1;
+                if constexpr (cz == -1) wall = wall || z == 0;
+                if constexpr (cz == 1) wall = wall || z == g.nz - 1;
+            } else {
+                if constexpr (cx == -1) tx = x == 0 ? g.nxl - 1 : tx;
+                if constexpr (cx == 1) tx = x == g.nxl - 1 ? 0 : tx;
+                if constexpr (cy == -1) ty = y == 0 ? g.ny - 1 : ty;
+                if constexpr (cy == 1) ty = y == g.ny - 1 ? 0 : ty;
+                if constexpr (cz == -1) tz = z == 0 ? g.nz - 1 : tz;
+                if constexpr (cz == 1) tz = z == g.nz - 1 ? 0 : tz;
+            }
+            if (!wall) {
+                T rn, uxn, uyn, uzn;
+                k0_load<T>(rho, u, cell_of(tx, ty, tz), rn, uxn, uyn, uzn);
+                v = feq_dir<T, j>(rn, uxn, uyn, uzn);
+            } else {
+                constexpr int ko = slot_opp(k);
+                v = feq[can_opp(j)];
+                if constexpr (cz == 1) {
+                    if (z == g.nz - 1) v = v - P.lid[ko];
+                }
+            }
+        }
+        A[self + (long long)k * g.pq] = v;
+    });
+}
+
 // Import canonical host-order doubles f[19][nx_c][ny][nz] (a chunk of nx_c
 // planes starting at slab-local xbeg) into slot layout C.
 template <typename T>
@@ -187,6 +283,16 @@ cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, cons
 }
 
 template <typename T>
+cudaError_t launch_k0_init_pull(const double* rho, const double* u, T* A, const StepParams<T>& P, cudaStream_t s) {
+    const SlabGeom& g = P.g;
+    if (g.bc == BC_PERIODIC)
+        k0_init_pull<T, BC_PERIODIC><<<cell_grid(g.nz, g.ny, g.nxl), kBlock, 0, s>>>(rho, u, A, P);
+    else
+        k0_init_pull<T, BC_CAVITY><<<cell_grid(g.nz, g.ny, g.nxl), kBlock, 0, s>>>(rho, u, A, P);
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_k0_unstream(const T* C, T* A, const StepParams<T>& P, cudaStream_t s) {
     if (P.g.bc == BC_PERIODIC)
         k0_unstream<T, BC_PERIODIC><<<cell_grid(P.g.nz, P.g.ny, P.g.nxl), kBlock, 0, s>>>(C, A, P);
@@ -226,6 +332,8 @@ cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int 
     template cudaError_t launch_k0_equilibrium<T>(const double*, const double*, T*, const SlabGeom&,         \
                                                   cudaStream_t, int, int);                                   \
     template cudaError_t launch_k0_unstream<T>(const T*, T*, const StepParams<T>&, cudaStream_t);            \
+    template cudaError_t launch_k0_init_pull<T>(const double*, const double*, T*, const StepParams<T>&,      \
+                                                cudaStream_t);                                               \
     template cudaError_t launch_k0_import<T>(const double*, T*, const SlabGeom&, int, int, cudaStream_t);    \
     template cudaError_t launch_k3_materialize<T>(const T*, const StepParams<T>&, int, int, int, int, int,   \
                                                   int, double*, cudaStream_t);                               \

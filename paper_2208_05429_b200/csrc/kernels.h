@@ -41,6 +41,9 @@ cudaError_t launch_aa_merge(T* dst, const T* src, const SlabGeom& g, int slot0, 
 template <typename T>
 cudaError_t launch_aa_moments(const T* F, const StepParams<T>& P, bool odd, int xbeg, int nxc, double* rho,
                               double* u, cudaStream_t s);
+// K0 fused, one slab spanning the domain: the pull-form state from rho, u
+template <typename T>
+cudaError_t launch_k0_init_pull(const double* rho, const double* u, T* A, const StepParams<T>& P, cudaStream_t s);
 template <typename T>
 cudaError_t launch_k0_unstream(const T* C, T* A, const StepParams<T>& P, cudaStream_t s);
 template <typename T>
