@@ -172,7 +172,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "k1", "k2", "k2reg", "aa"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "k1", "k2", "k2reg", "aa", "k2sc"])
     ap.add_argument("--lbm-steps", type=int, default=None, help="time steps per job (default: the config's)")
     ap.add_argument("--dims", default=None, help="override NX,NY,NZ (profiling runs only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -210,7 +210,7 @@ def main():
     cells_local = nxl * cfg.ny * cfg.nz
     stream = torch.cuda.Stream(device=dev)
     kernel = {"auto": lbm.LBM_KERNEL_AUTO, "k1": lbm.LBM_KERNEL_K1, "k2": lbm.LBM_KERNEL_K2, "k2reg": lbm.LBM_KERNEL_K2_REG,
-              "aa": lbm.LBM_KERNEL_AA}[args.kernel]
+              "aa": lbm.LBM_KERNEL_AA, "k2sc": lbm.LBM_KERNEL_K2_SC}[args.kernel]
 
     nccl_id = None
     if world > 1:

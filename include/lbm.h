@@ -95,7 +95,19 @@ typedef enum {
      * and after each odd step; cavity slabs need >= 2 planes (EINVAL).
      * Bitwise identical to K1 without a lid (with it, K1's pull storage
      * rounds the lid term once more: agreement to ~1 ulp). */
-    LBM_KERNEL_AA = 4
+    LBM_KERNEL_AA = 4,
+    /* Single-copy storage with the two-step merge -- the paper's pairing of
+     * one lattice copy with two steps per pass (
+     * SURVEY.md 8(f) row 1).  The K2 sweep runs in place: the lattice is a
+     * ring of nx + 4 + G planes (G = 68 fp64 / 100 fp32; 1.07x a single copy
+     * at nx = 1024, plus a staging buffer of max(3 planes, 64 MB, 1/16 of the
+     * lattice) for host transfers) and each sweep writes f*(t+1) of plane x
+     * G planes below the slot of f*(t-1) of plane x, chunks of <= 32 (48)
+     * planes taken in x order, so no plane is overwritten before its last
+     * reader has finished; an odd step runs the in-place K1 the same way.
+     * Bitwise identical to K2/K1.  EINVAL at create unless world == 1 and
+     * local_slabs == 1, or where the TMA descriptor cannot describe the slab. */
+    LBM_KERNEL_K2_SC = 5
 } lbm_kernel;
 
 /* Halo transport between X-slabs (PAPER.md:336 X-only partition).

@@ -98,6 +98,12 @@ struct lbm_ctx {
     bool aa = false, aa_odd = false;
     void* stage = nullptr;
     size_t stage_bytes = 0;
+    // single-copy two-step storage (LBM_KERNEL_K2_SC): buf[0] is a ring of
+    // pmod plane slots, the state window at slot g.poff; in-place sweeps
+    // shift it down by sc_gap (K2) or kK1ScGap (K1) slots
+    bool sc = false;
+    int sc_gap = 0;
+    unsigned* sc_sync = nullptr;
     ncclComm_t comm = nullptr;
     size_t esize = 8;
     int* d_flag = nullptr;
@@ -194,7 +200,29 @@ StepParams<T> make_params(const lbm_ctx* c, const Slab& s) {
 }
 
 // ---------------------------------------------------------------- halo --
+// Single-copy ring (one slab, periodic): the x wrap onto itself, plane by
+// plane through the ring mapping -- right ghost [x=nxl: all | x=nxl+1: M]
+// <- [x=0 | x=1], left ghost [x=-2: P | x=-1: all] <- [x=nxl-2 | x=nxl-1].
+lbm_status exchange_sc(lbm_ctx* c, cudaStream_t st) {
+    Slab& s = c->slabs[0];
+    const SlabGeom& g = s.g;
+    char* b = static_cast<char*>(s.buf[0]);
+    const size_t es = c->esize;
+    auto copy = [&](int xd, int xs, int slot0, int nslots) -> cudaError_t {
+        const long long o = (long long)slot0 * g.pq;
+        return cudaMemcpyAsync(b + (plane_base(g, xd) + o) * es, b + (plane_base(g, xs) + o) * es,
+                               size_t(nslots) * g.pq * es, cudaMemcpyDeviceToDevice, st);
+    };
+    const int n = g.nxl;
+    CK(copy(n, 0, 0, kQ));
+    CK(copy(n + 1, 1, 0, kSlotsM));
+    CK(copy(-2, n - 2, kSlotP0, kQ - kSlotP0));
+    CK(copy(-1, n - 1, 0, kQ));
+    return LBM_OK;
+}
+
 lbm_status exchange(lbm_ctx* c, int which, cudaStream_t st) {
+    if (c->sc) return exchange_sc(c, st);
     if (c->opts.comm == LBM_COMM_NCCL) {
         Slab& s = c->slabs[0];
         char* b = static_cast<char*>(s.buf[which]);
@@ -401,9 +429,41 @@ lbm_status run_steps_aa(lbm_ctx* c, long n) {
     return LBM_OK;
 }
 
+// single-copy ring storage: K2 sweeps in place (k2.cu), an odd remainder
+// by the in-place K1; each shifts the state window down the ring
+template <typename T>
+lbm_status run_steps_sc(lbm_ctx* c, long n) {
+    Slab& s = c->slabs[0];
+    T* F = static_cast<T*>(s.buf[0]);
+    while (n > 0) {
+        const int nsteps = n >= 2 ? 2 : 1;
+        lbm_status st = ensure_ghosts(c);
+        if (st != LBM_OK) return st;
+        size_t slot = 0;
+        st = prof_begin(c, slot);
+        if (st != LBM_OK) return st;
+        const StepParams<T> P = make_params<T>(c, s);
+        const int shift = nsteps == 2 ? c->sc_gap : kK1ScGap;
+        const int out_poff = (s.g.poff - shift + s.g.pmod) % s.g.pmod;
+        cudaError_t e = nsteps == 2 ? launch_k2<T>(F, F, P, 0, s.g.nxl, c->stream, out_poff, c->sc_sync)
+                                    : launch_k1_sc<T>(F, P, out_poff, c->sc_sync, c->stream);
+        if (e != cudaSuccess) return fail(c, LBM_ECUDA, "single-copy sweep launch failed: %s", cudaGetErrorString(e));
+        c->launches++;
+        (nsteps == 2 ? c->k2_launches : c->k1_launches)++;
+        st = prof_end(c, slot, (long long)nsteps * s.g.nxl * s.g.ny * s.g.nz);
+        if (st != LBM_OK) return st;
+        s.g.poff = out_poff;
+        c->ghosts_valid = false;
+        c->t += nsteps;
+        n -= nsteps;
+    }
+    return LBM_OK;
+}
+
 template <typename T>
 lbm_status run_steps(lbm_ctx* c, long n) {
     if (c->aa) return run_steps_aa<T>(c, n);
+    if (c->sc) return run_steps_sc<T>(c, n);
     // AUTO and K2: the TMA-staged two-step sweep (k2.cu) where the TMA
     // descriptor can describe the slab, else the cp.async-staged one (K2R,
     // k2r.cu); K2_REG forces K2R.  AUTO falls back to K1 pairs when neither
@@ -568,9 +628,114 @@ lbm_status init_eq_aa(lbm_ctx* c, const double* rho, const double* u, bool host)
     return finish_init<T>(c, 0);
 }
 
+// Host-staged x windows of the single-copy ring's init / import: planes
+// [xb, xb + nxc) need their x neighbours, so a chunk stages the planes
+// xb - 1 .. xb + nxc (mod nxl) -- a contiguous run of host planes, or two
+// where it wraps -- as `per_cell` doubles per cell in every one of `rows`
+// row blocks of host stride `row_stride` cells.
+struct ScWindow {
+    int w0, wn;
+};
+ScWindow sc_window(const SlabGeom& g, int xb, int nxc) {
+    if (g.nxl == 1 || nxc == g.nxl) return {0, g.nxl};
+    if (g.bc == BC_PERIODIC) return {(xb - 1 + g.nxl) % g.nxl, std::min(nxc + 2, g.nxl)};
+    const int a = std::max(0, xb - 1), b = std::min(g.nxl, xb + nxc + 1);
+    return {a, b - a};
+}
+
+lbm_status sc_stage_window(lbm_ctx* c, const double* host, ScWindow w, long long plane, int per_cell, int rows,
+                           long long row_stride, double* dst) {
+    const SlabGeom& g = c->slabs[0].g;
+    const int n1 = std::min(w.wn, g.nxl - w.w0);  // planes before the wrap
+    const size_t dpitch = size_t(w.wn) * plane * per_cell * sizeof(double);
+    const size_t spitch = size_t(row_stride) * per_cell * sizeof(double);
+    CK(cudaMemcpy2DAsync(dst, dpitch, host + (long long)w.w0 * plane * per_cell, spitch,
+                         size_t(n1) * plane * per_cell * sizeof(double), rows, cudaMemcpyHostToDevice, c->stream));
+    if (n1 < w.wn)
+        CK(cudaMemcpy2DAsync(dst + (long long)n1 * plane * per_cell, dpitch, host, spitch,
+                             size_t(w.wn - n1) * plane * per_cell * sizeof(double), rows, cudaMemcpyHostToDevice,
+                             c->stream));
+    return LBM_OK;
+}
+
+template <typename T>
+lbm_status sc_init_done(lbm_ctx* c) {
+    c->cur = 0;
+    c->ghosts_valid = false;
+    c->initialized = true;
+    c->t = 0;
+    return LBM_OK;
+}
+
+template <typename T>
+lbm_status init_eq_sc(lbm_ctx* c, const double* rho, const double* u, bool host) {
+    Slab& s = c->slabs[0];
+    const StepParams<T> P = make_params<T>(c, s);
+    T* F = static_cast<T*>(s.buf[0]);
+    if (!host) {
+        CK(launch_k0_init_pull<T>(rho, u, nullptr, F, P, 0, s.g.nxl, 0, s.g.nxl, c->stream));
+        c->launches++;
+        return sc_init_done<T>(c);
+    }
+    const long long plane = (long long)c->ny * c->nz;
+    // planes per chunk: 32 B (rho + u) per cell, two halo planes
+    const int cap = int(std::max<long long>(1, (long long)(c->stage_bytes / (4 * sizeof(double))) / plane - 2));
+    double* stage = static_cast<double*>(c->stage);
+    for (int xb = 0; xb < s.g.nxl; xb += cap) {
+        const int nxc = std::min(cap, s.g.nxl - xb);
+        const ScWindow w = sc_window(s.g, xb, nxc);
+        const long long cells = (long long)w.wn * plane;
+        const double* dr = nullptr;
+        const double* du = nullptr;
+        lbm_status st;
+        if (rho) {
+            if ((st = sc_stage_window(c, rho, w, plane, 1, 1, s.g.nxl * plane, stage)) != LBM_OK) return st;
+            dr = stage;
+        }
+        if (u) {
+            if ((st = sc_stage_window(c, u, w, plane, 3, 1, s.g.nxl * plane, stage + cells)) != LBM_OK) return st;
+            du = stage + cells;
+        }
+        int flag = 0;
+        if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
+        if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+        if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
+        if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+        CK(launch_k0_init_pull<T>(dr, du, nullptr, F, P, xb, nxc, w.w0, w.wn, c->stream));
+        c->launches++;
+    }
+    return sc_init_done<T>(c);
+}
+
+template <typename T>
+lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
+    Slab& s = c->slabs[0];
+    const StepParams<T> P = make_params<T>(c, s);
+    T* F = static_cast<T*>(s.buf[0]);
+    const long long plane = (long long)c->ny * c->nz;
+    const int cap =
+        int(std::max<long long>(1, (long long)(c->stage_bytes / (kQ * sizeof(double))) / plane - 2));
+    double* stage = static_cast<double*>(c->stage);
+    c->initialized = false;
+    for (int xb = 0; xb < s.g.nxl; xb += cap) {
+        const int nxc = std::min(cap, s.g.nxl - xb);
+        const ScWindow w = sc_window(s.g, xb, nxc);
+        lbm_status st = sc_stage_window(c, f, w, plane, 1, kQ, (long long)s.g.nxl * plane, stage);
+        if (st != LBM_OK) return st;
+        int flag = 0;
+        st = validate_device(c, stage, (long long)kQ * w.wn * plane, false, &flag);
+        if (st != LBM_OK) return st;
+        if (flag) return fail(c, LBM_EINVAL, "populations must be finite (state is now undefined)");
+        CK(launch_k0_init_pull<T>(nullptr, nullptr, stage, F, P, xb, nxc, w.w0, w.wn, c->stream));
+        c->launches++;
+    }
+    return sc_init_done<T>(c);
+}
+
 template <typename T>
 lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
     if (c->aa) return init_eq_aa<T>(c, rho, u, host);
+    if (c->sc) return init_eq_sc<T>(c, rho, u, host);
     const long long plane = (long long)c->ny * c->nz;
     const int canon = c->cur;  // canonical f(t0) is built here, the state ends in the other buffer
     for (Slab& s : c->slabs) {
@@ -603,7 +768,8 @@ lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
         if (c->slabs.size() == 1 && c->opts.world == 1) {
             // one slab spanning the domain: the pull-form state in one pass
             // (k0_init_pull), the staging (host inputs) in the other buffer
-            CK(launch_k0_init_pull<T>(dr, du, static_cast<T*>(s.buf[canon]), make_params<T>(c, s), c->stream));
+            CK(launch_k0_init_pull<T>(dr, du, nullptr, static_cast<T*>(s.buf[canon]), make_params<T>(c, s), 0,
+                                      s.g.nxl, 0, s.g.nxl, c->stream));
             c->launches++;
             c->cur = canon;
             c->ghosts_valid = false;
@@ -619,6 +785,7 @@ lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
 
 template <typename T>
 lbm_status set_pops(lbm_ctx* c, const double* f) {
+    if (c->sc) return set_pops_sc<T>(c, f);
     const long long plane = (long long)c->ny * c->nz;
     const long long proc_cells = (long long)c->nxl_proc * plane;
     // import into the non-state buffer, stage in the state buffer (AA: into
@@ -656,10 +823,14 @@ lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
     for (Slab& s : c->slabs) {
         const StepParams<T> P = make_params<T>(c, s);
         const T* F = static_cast<const T*>(s.buf[0]);
+        // AA: the phase-aware moments; single-copy ring: K3 on the window
+        auto moments = [&](int xb, int nxc, double* r, double* v) {
+            return c->sc ? launch_k3_moments<T>(F, P, xb, nxc, r, v, c->stream)
+                         : launch_aa_moments<T>(F, P, c->aa_odd, xb, nxc, r, v, c->stream);
+        };
         const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;
         if (!host) {
-            CK(launch_aa_moments<T>(F, P, c->aa_odd, 0, s.g.nxl, rho ? rho + xoff : nullptr,
-                                    u ? u + 3 * xoff : nullptr, c->stream));
+            CK(moments(0, s.g.nxl, rho ? rho + xoff : nullptr, u ? u + 3 * xoff : nullptr));
             c->launches++;
             continue;
         }
@@ -667,8 +838,7 @@ lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
             const int nxc = std::min(cap, s.g.nxl - xb);
             const long long cells = (long long)nxc * plane;
             const long long hoff = xoff + (long long)xb * plane;
-            CK(launch_aa_moments<T>(F, P, c->aa_odd, xb, nxc, rho ? stage : nullptr, u ? stage + cells : nullptr,
-                                    c->stream));
+            CK(moments(xb, nxc, rho ? stage : nullptr, u ? stage + cells : nullptr));
             c->launches++;
             if (rho)
                 CK(cudaMemcpyAsync(rho + hoff, stage, cells * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -683,7 +853,7 @@ lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
 
 template <typename T>
 lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
-    if (c->aa) return macro_aa<T>(c, rho, u, host);
+    if (c->aa || c->sc) return macro_aa<T>(c, rho, u, host);
     lbm_status st = ensure_ghosts(c);
     if (st != LBM_OK) return st;
     const long long plane = (long long)c->ny * c->nz;
@@ -724,8 +894,8 @@ lbm_status get_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, d
         const int a = std::max(bx, sx0), b = std::min(bx + lx, sx0 + s.g.nxl);
         if (a >= b) continue;
         const StepParams<T> P = make_params<T>(c, s);
-        double* stage = static_cast<double*>(c->aa ? c->stage : s.buf[c->cur ^ 1]);
-        const size_t stage_bytes = c->aa ? c->stage_bytes : size_t(s.plan.buffer_elems) * c->esize;
+        double* stage = static_cast<double*>(c->stage ? c->stage : s.buf[c->cur ^ 1]);
+        const size_t stage_bytes = c->stage ? c->stage_bytes : size_t(s.plan.buffer_elems) * c->esize;
         const long long cap_planes =
             std::max<long long>(1, (long long)stage_bytes / (kQ * bplane * (long long)sizeof(double)));
         for (int xb = a; xb < b; xb += int(cap_planes)) {
@@ -820,7 +990,9 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         return fail(c, LBM_EINVAL, "comm NCCL needs local_slabs == 1 and an nccl_id");
     if (o.comm == LBM_COMM_LOCAL && o.world != 1) return fail(c, LBM_EINVAL, "comm LOCAL needs world == 1");
     if (o.comm < LBM_COMM_NONE || o.comm > LBM_COMM_LOCAL) return fail(c, LBM_EINVAL, "bad comm %d", o.comm);
-    if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_AA) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K2_SC) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    if (o.kernel == LBM_KERNEL_K2_SC && (o.world != 1 || o.local_slabs != 1))
+        return fail(c, LBM_EINVAL, "kernel K2_SC needs a single slab (world == 1, local_slabs == 1)");
     if (o.kernel == LBM_KERNEL_AA && o.bc == LBM_BC_CAVITY && (o.world > 1 || o.local_slabs > 1) &&
         nx / (o.world * o.local_slabs) < 2)
         return fail(c, LBM_EINVAL, "kernel AA with X-slabs needs >= 2 planes per slab");
@@ -870,6 +1042,15 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         s.g.pq = s.plan.plane_q;
         s.g.px = s.plan.plane_x;
         s.g.bc = o.bc;
+        s.g.poff = 0;
+        s.g.pmod = nxl + 4;
+        if (o.kernel == LBM_KERNEL_K2_SC) {
+            c->sc = true;
+            c->sc_gap = dt == LBM_F64 ? k2_sc_gap<double>() : k2_sc_gap<float>();
+            s.g.pmod = nxl + 4 + c->sc_gap;
+            const bool ok = dt == LBM_F64 ? k2_supported<double>(s.g) : k2_supported<float>(s.g);
+            if (!ok) return bail(fail(c, LBM_EINVAL, "kernel K2_SC: the TMA descriptor cannot describe this slab"));
+        }
         // cavity chain: only the outer faces of the first and last slab are walls
         s.g.left_wall = (o.bc == LBM_BC_CAVITY && grank == 0);
         s.g.right_wall = (o.bc == LBM_BC_CAVITY && grank == nslab_total - 1);
@@ -881,8 +1062,8 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
             s.left = s.plan.left >= 0 ? s.plan.left - o.rank * sw : -1;
             s.right = s.plan.right >= 0 ? s.plan.right - o.rank * sw : -1;
         }
-        const size_t bytes = size_t(s.plan.buffer_elems) * c->esize;
-        for (int b = 0; b < (o.kernel == LBM_KERNEL_AA ? 1 : 2); ++b) {
+        const size_t bytes = size_t(s.g.pmod) * size_t(s.plan.plane_x) * c->esize;
+        for (int b = 0; b < (c->sc || o.kernel == LBM_KERNEL_AA ? 1 : 2); ++b) {
             cudaError_t e = cudaMalloc(&s.buf[b], bytes);
             if (e != cudaSuccess) {
                 cudaGetLastError();
@@ -893,13 +1074,18 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         }
     }
     if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess) return bail(fail(c, LBM_ENOMEM, "cudaMalloc flag"));
-    if (o.kernel == LBM_KERNEL_AA) {
-        // host transfers are staged plane-chunk by plane-chunk: >= one plane
-        // of 19 doubles, 64 MB or 1/16 of the lattice, whichever is larger
-        c->aa = true;
+    if (c->sc && cudaMalloc(&c->sc_sync, sizeof(unsigned) * (size_t(nxl) + 1)) != cudaSuccess)
+        return bail(fail(c, LBM_ENOMEM, "cudaMalloc ring tickets"));
+    if (o.kernel == LBM_KERNEL_AA || c->sc) {
+        // host transfers are staged plane-chunk by plane-chunk: >= three planes
+        // of 19 doubles (a plane and its x halo), 64 MB or 1/16 of the
+        // lattice, whichever is larger
+        c->aa = !c->sc;
         const size_t plane19 = size_t(kQ) * ny * nz * sizeof(double);
         const size_t lattice = size_t(c->slabs[0].plan.buffer_elems) * c->esize;
-        c->stage_bytes = std::max({plane19, size_t(64) << 20, lattice / 16});
+        c->stage_bytes = std::max({3 * plane19, size_t(64) << 20, lattice / 16});
+        if (const char* e = getenv("LBM_STAGE_BYTES"))  // tests: force multi-chunk host transfers
+            c->stage_bytes = std::max(3 * plane19, size_t(atoll(e)));
         if (cudaMalloc(&c->stage, c->stage_bytes) != cudaSuccess) {
             cudaGetLastError();
             return bail(fail(c, LBM_ENOMEM, "cudaMalloc staging (%zu bytes)", c->stage_bytes));
@@ -953,6 +1139,7 @@ void lbm_destroy(lbm_ctx* c) {
         for (void* b : s.buf)
             if (b) cudaFree(b);
     if (c->d_flag) cudaFree(c->d_flag);
+    if (c->sc_sync) cudaFree(c->sc_sync);
     if (c->stage) cudaFree(c->stage);
     if (c->comm_stream) {
         cudaStreamSynchronize(c->comm_stream);

@@ -144,10 +144,10 @@ __device__ __forceinline__ int wrapi(int v, int n) {
 
 }  // namespace
 
-template <typename T, int BC, int TY, int TZ, bool EARLY>
+template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
 __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     k2_sweep(const __grid_constant__ CUtensorMap tmA, const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
-             int xbeg, int xend, int chunk) {
+             int xbeg, int xend, int chunk, int out_poff, unsigned* __restrict__ sc_sync) {
     using C = K2Cfg<T, TY, TZ>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* const stage = reinterpret_cast<T*>(smem_raw);
@@ -158,12 +158,53 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     uint64_t* const bar = reinterpret_cast<uint64_t*>(wallbuf + 2 * C::WALLE);
 
     const SlabGeom& g = P.g;
+    // Work item (tile, x chunk): the block index, or -- single-copy ring
+    // storage, where step 2 overwrites planes of f*(t-1) in place -- a ticket
+    // taken in chunk-major order.  There the outputs of chunk j land on the
+    // input planes of chunks <= j - 2 (launch_k2), so a CTA of chunk j first
+    // waits until every CTA of chunks j - 2 and j - 3 has finished -- which,
+    // by induction over those CTAs' own waits, means every chunk <= j - 2.
+    // The awaited CTAs hold earlier tickets, so they are running or done: no
+    // deadlock.  (A persistent variant -- CTAs looping over tickets, the TMA
+    // of the next item's first planes issued while the current one drains --
+    // measured slower: 35.3k vs 36.4k MLUPS fp64.)
+    int item_t = int(blockIdx.x), item_c = int(blockIdx.y);
+    if (RING) {
+        int* const s_item = reinterpret_cast<int*>(smem_raw);
+        if (threadIdx.x == 0) {
+            const unsigned it = atomicAdd(&sc_sync[0], 1u);
+            const int ch = int(it / gridDim.x);
+            for (int back = 2; back <= 3; ++back)
+                if (ch >= back) sc_wait(&sc_sync[1 + ch - back], gridDim.x);
+            *s_item = int(it);
+        }
+        __syncthreads();
+        item_t = *s_item % int(gridDim.x);
+        item_c = *s_item / int(gridDim.x);
+    }
+    // single-copy ring: this CTA's stores are complete and visible -> count
+    // it (the chunk index recomputed from xs: nothing extra live in the loop)
+    auto sc_finish = [&](int xs_) {
+        if (RING) {
+            // the barrier orders every thread's stores before thread 0's
+            // cumulative gpu-scope fence, then the count (the pattern of a
+            // cooperative grid barrier)
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(&sc_sync[1 + (xs_ - xbeg) / chunk], 1u);
+            }
+        }
+    };
     const int ntz = (g.nz + TZ - 1) / TZ;
-    const int y0 = (int(blockIdx.x) / ntz) * TY;
-    const int z0 = (int(blockIdx.x) % ntz) * TZ;
-    const int xs = xbeg + int(blockIdx.y) * chunk;
+    const int y0 = (item_t / ntz) * TY;
+    const int z0 = (item_t % ntz) * TZ;
+    const int xs = xbeg + item_c * chunk;
     const int xe = min(xs + chunk, xend);
-    if (xs >= xe) return;
+    if (xs >= xe) {
+        sc_finish(xs);
+        return;
+    }
     // step-1 planes: one beyond each end of the chunk unless that is beyond a wall
     const int p_first = (xs == 0 && BC == BC_CAVITY && g.left_wall) ? 0 : xs - 1;
     const int p_last = (xe == g.nxl && BC == BC_CAVITY && g.right_wall) ? g.nxl - 1 : xe;
@@ -202,7 +243,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
             constexpr int k = decltype(kc)::value;
             constexpr int i = slot_dir(k);
             tma_load_3d(stage + (s * kQ + k) * C::BOXE, &tmA, &bar[s], z0 - C::ZPAD, y0 - 1 - can_cy(i),
-                        (p - can_cx(i) + 2) * kQ + k);
+                        plane_slot_t<RING>(g, p - can_cx(i)) * kQ + k);
         });
     };
 
@@ -242,7 +283,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool wl_row = wb_ok && q_in && a == wrow, wl_col = wb_ok && q_in && b == wcol;
     auto wall_prefetch = [&](int pn, int buf) {  // this thread's wall values of plane pn
         if (!(wl_row || wl_col)) return;
-        const T* const selfp = A + cell_off(g, pn, qy, qz);
+        const T* const selfp = A + plane_base_t<RING>(g, pn) + (long long)qy * g.nzp + qz;
         T* const wb = wallbuf + buf * C::WALLE;
         static_for<0, kQ>([&](auto kc) {
             constexpr int k = decltype(kc)::value;
@@ -312,7 +353,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                             constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
                             const int sy = qy - cy, sz = qz - cz;
                             if (sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz)
-                                fs[i] = A[(long long)(p - cx + 2) * g.px + (long long)k * g.pq +
+                                fs[i] = A[plane_base_t<RING>(g, p - cx) + (long long)k * g.pq +
                                           (long long)wrapi(sy, g.ny) * g.nzp + wrapi(sz, g.nz)];
                         });
                     }
@@ -357,7 +398,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                         if (p + 1 <= p_last) wall_prefetch(p + 1, (c + 1) & 1);
                     } else if ((edge_tile || lwall || rwall) && q_in) {
                         if (wb_ok && p + 1 <= p_last) wall_prefetch(p + 1, (c + 1) & 1);
-                        const long long self = cell_off(g, p, qy, qz);
+                        const long long self = plane_base_t<RING>(g, p) + (long long)qy * g.nzp + qz;
                         static_for<0, kQ>([&](auto kc) {
                             constexpr int k = decltype(kc)::value;
                             constexpr int i = slot_dir(k);
@@ -413,7 +454,12 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         if (do2 && in2) {
             // slot-plane bases are CTA-uniform (uniform datapath); the
             // thread adds its 32-bit in-plane offset: one IMAD.WIDE per store
-            T* const Bd = B + (long long)(d + 2) * g.px;
+            int dslot = d + 2;  // ring slot of the output plane
+            if constexpr (RING) {
+                dslot += out_poff;
+                dslot = dslot >= g.pmod ? dslot - g.pmod : dslot;
+            }
+            T* const Bd = B + (long long)dslot * g.px;
             static_for<0, kQ>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
                 __stcs(Bd + (long long)k * g.pq + st_off, f2[slot_dir(k)]);
@@ -484,6 +530,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
             if (tid == 0 && has1 && p + 2 <= p_last) issue(p + 2, s);
         }
     }
+    sc_finish(xs);
 }
 
 // ------------------------------------------------------------------ host --
@@ -536,11 +583,18 @@ int num_sms() {
     return n;
 }
 
-template <typename T, int BC, int TY, int TZ, bool EARLY>
-cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
+// x chunks of at most k2_max_chunk planes (launch_k2_impl)
+template <typename T>
+constexpr int k2_max_chunk() {
+    return sizeof(T) == 8 ? 32 : 48;
+}
+
+template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
+cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, int out_poff,
+                           unsigned* sc_sync, cudaStream_t s) {
     using C = K2Cfg<T, TY, TZ>;
     constexpr int NT = C::NT;
-    auto kern = k2_sweep<T, BC, TY, TZ, EARLY>;
+    auto kern = k2_sweep<T, BC, TY, TZ, EARLY, RING>;
     static int occ = -1;
     if (occ < 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -553,7 +607,7 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     if (!enc) return cudaErrorNotSupported;
     const SlabGeom& g = P.g;
     CUtensorMap map;
-    const cuuint64_t dims[3] = {cuuint64_t(g.nz), cuuint64_t(g.ny), cuuint64_t(g.nxl + 4) * kQ};
+    const cuuint64_t dims[3] = {cuuint64_t(g.nz), cuuint64_t(g.ny), cuuint64_t(g.pmod) * kQ};
     const cuuint64_t strides[2] = {cuuint64_t(g.nzp) * sizeof(T), cuuint64_t(g.pq) * sizeof(T)};
     const cuuint32_t box[3] = {cuuint32_t(C::BW), cuuint32_t(C::HY), 1u};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
@@ -584,7 +638,7 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     // ~2.5 planes of step 1.
     // fp32 tiles (16x32) re-read relatively less x-halo per plane: 48 planes
     // measured best there (65.9k -> 67.4k), 32 for fp64 (37.4k vs 36.9k)
-    constexpr int kMaxChunk = sizeof(T) == 8 ? 32 : 48;
+    constexpr int kMaxChunk = k2_max_chunk<T>();
     int best = 1;
     double best_cost = 1e300;
     for (int nch = 1; nch <= nxs; ++nch) {
@@ -605,8 +659,13 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
         return e ? atoi(e) : 0;
     }();
     if (force_chunk > 0) chunk = min(force_chunk, nxs);
+    if (sc_sync) chunk = min(chunk, kMaxChunk);  // the ring gap assumes it (k2_sc_gap)
     const dim3 grid(unsigned(ntiles), unsigned((nxs + chunk - 1) / chunk));
-    kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk);
+    if (sc_sync) {  // tickets and per-chunk completion counters start at zero
+        cudaError_t e = cudaMemsetAsync(sc_sync, 0, sizeof(unsigned) * (1 + grid.y), s);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk, out_poff, sc_sync);
     return cudaGetLastError();
 }
 
@@ -617,11 +676,27 @@ bool k2_supported(const SlabGeom& g) {
     if (!get_encode()) return false;
     // TMA: row pitch a multiple of 16 B (nzp is padded to 32 B); the combined
     // (x, slot) dimension and the boxes fit the descriptor limits.
-    return (g.nzp * sizeof(T)) % 16 == 0 && (long long)(g.nxl + 4) * kQ < (1LL << 31) && g.nxl >= 1;
+    return (g.nzp * sizeof(T)) % 16 == 0 && (long long)g.pmod * kQ < (1LL << 31) && g.nxl >= 1;
+}
+
+// Single-copy ring (launch_k2 with sc_sync): a sweep writes f*(t+1) of plane
+// d into the ring slot of input plane d - gap.  With chunks of L <= k2_max_chunk
+// planes, chunk j writes input planes [jL - gap, (j+1)L - gap), which chunk
+// j-1 and later no longer read iff gap >= 2L + 2 ([jL - 2, (j+1)L + 1] is
+// what chunk j reads); chunks <= j-2 have finished (the ticket wait).
+template <typename T>
+int k2_sc_gap() {
+    return 2 * k2_max_chunk<T>() + 4;
 }
 
 template <typename T>
-cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
+int k2_sc_max_chunks(int nxl) {
+    return nxl;  // chunks of >= 1 plane
+}
+
+template <typename T>
+cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s, int out_poff,
+                      unsigned* sc_sync) {
     if (nxs <= 0) return cudaSuccess;
     const bool per = P.g.bc == BC_PERIODIC;
     // Default: read the stage into registers and issue the next TMA before
@@ -633,15 +708,20 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
         const char* e = getenv("LBM_K2_EARLY");
         return !(e && e[0] == '0');
     }();
-#define LBM_K2_TILE_CASE(TY, TZ)                                                         \
-    if constexpr (K2Cfg<T, TY, TZ>::FITS) {                                              \
-        if (early)                                                                       \
-            return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true>(A, B, P, xbeg, nxs, s) \
-                       : launch_k2_impl<T, BC_CAVITY, TY, TZ, true>(A, B, P, xbeg, nxs, s);  \
-        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, false>(A, B, P, xbeg, nxs, s)    \
-                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, false>(A, B, P, xbeg, nxs, s);     \
-    } else {                                                                             \
-        return cudaErrorInvalidConfiguration;                                            \
+    if (sc_sync) {  // single-copy ring storage: the default shape only
+        constexpr int TY = sizeof(T) == 8 ? 8 : 16, TZ = 32;
+        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, true>(A, B, P, xbeg, nxs, out_poff, sc_sync, s)
+                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, true>(A, B, P, xbeg, nxs, out_poff, sc_sync, s);
+    }
+#define LBM_K2_TILE_CASE(TY, TZ)                                                                              \
+    if constexpr (K2Cfg<T, TY, TZ>::FITS) {                                                                   \
+        if (early)                                                                                            \
+            return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, s) \
+                       : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, s);  \
+        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, s)    \
+                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, s);     \
+    } else {                                                                                                  \
+        return cudaErrorInvalidConfiguration;                                                                 \
     }
     switch (tile_choice(sizeof(T))) {
         case 1: LBM_K2_TILE_CASE(8, 32);
@@ -660,7 +740,13 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
 
 template bool k2_supported<double>(const SlabGeom&);
 template bool k2_supported<float>(const SlabGeom&);
-template cudaError_t launch_k2<double>(const double*, double*, const StepParams<double>&, int, int, cudaStream_t);
-template cudaError_t launch_k2<float>(const float*, float*, const StepParams<float>&, int, int, cudaStream_t);
+template cudaError_t launch_k2<double>(const double*, double*, const StepParams<double>&, int, int, cudaStream_t,
+                                       int, unsigned*);
+template cudaError_t launch_k2<float>(const float*, float*, const StepParams<float>&, int, int, cudaStream_t, int,
+                                      unsigned*);
+template int k2_sc_gap<double>();
+template int k2_sc_gap<float>();
+template int k2_sc_max_chunks<double>(int);
+template int k2_sc_max_chunks<float>(int);
 
 }  // namespace lbm

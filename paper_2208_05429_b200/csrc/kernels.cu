@@ -32,6 +32,44 @@ __global__ void __launch_bounds__(256) k1_step(const T* __restrict__ A, T* __res
     });
 }
 
+// K1 on single-copy ring storage (LBM_KERNEL_K2_SC, odd remainders): one
+// step in place, f*(t) of plane x written into the ring slot of input plane
+// x - 4 (out_poff = poff - 4).  Tiles are taken by ticket in plane order; a
+// tile of plane x waits until planes x-3, x-4, x-5 are finished (so, by
+// induction, every plane <= x-3, the last readers of plane x-4).
+template <typename T, int BC>
+__global__ void __launch_bounds__(256) k1_step_sc(T* F, StepParams<T> P, int out_poff, unsigned* sync, int tiles_z,
+                                                 int tpp) {
+    __shared__ int s_item;
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        const unsigned it = atomicAdd(&sync[0], 1u);
+        const int x = int(it) / tpp;
+        for (int back = 3; back <= 5; ++back)
+            if (x >= back) sc_wait(&sync[1 + x - back], unsigned(tpp));
+        s_item = int(it);
+    }
+    __syncthreads();
+    const int x = s_item / tpp, tile = s_item % tpp;
+    const int z = (tile % tiles_z) * 32 + threadIdx.x;
+    const int y = (tile / tiles_z) * 8 + threadIdx.y;
+    if (z < P.g.nz && y < P.g.ny) {
+        T f[kQ];
+        pull_cell<T, BC>(F, P, x, y, z, f);
+        bgk_collide<T>(f, P.omega);
+        const int ps = x + 2 + out_poff;
+        T* const dst = F + (long long)(ps >= P.g.pmod ? ps - P.g.pmod : ps) * P.g.px + (long long)y * P.g.nzp + z;
+        static_for<0, kQ>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            __stcs(dst + (long long)k * P.g.pq, f[slot_dir(k)]);
+        });
+    }
+    __syncthreads();  // every thread's stores, then one cumulative fence and the count
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        __threadfence();
+        atomicAdd(&sync[1 + x], 1u);
+    }
+}
+
 // ------------------------------------------------------------ K0 init --
 // K0a: canonical f = feq(rho, u) of every slab cell into buffer C (slot
 // layout).  rho/u are double arrays [x][y][z] / [x][y][z][3] of the slab.
@@ -93,7 +131,7 @@ __global__ void __launch_bounds__(256) k0_unstream(const T* __restrict__ C, T* _
         }
         T v;
         if (!wall) {
-            v = C[(long long)(x + cx + 2) * g.px + (long long)k * g.pq + (long long)ty * g.nzp + tz];
+            v = C[plane_base(g, x + cx) + (long long)k * g.pq + (long long)ty * g.nzp + tz];
         } else {
             constexpr int ko = slot_opp(k);
             v = C[self + (long long)ko * g.pq];
@@ -146,19 +184,35 @@ __device__ __forceinline__ T feq_dir(T W, T ux, T uy, T uz) {
     return j <= 9 ? fma(C, cu, common) : fma(-C, cu, common);
 }
 
-template <typename T, int BC>
+// The x window of the per-cell inputs: plane index of slab plane tx (in
+// [0, nxl)) in a window holding planes wx0, wx0 + 1, ... (mod nxl) -- the
+// whole slab (wx0 = 0) or a host-staged chunk with its x halo.
+__device__ __forceinline__ long long k0_wcell(const SlabGeom& g, int wx0, int tx, int ty, int tz) {
+    int w = tx - wx0;
+    if (w < 0) w += g.nxl;
+    return ((long long)w * g.ny + ty) * g.nz + tz;
+}
+
+// IMPORT = false: f(t0) = feq(rho, u) (rho, u: 1 and 4 doubles per window
+// cell, either may be null); IMPORT = true: f(t0) given, canonical doubles
+// src[19][wn][ny][nz] (set_populations without a second lattice copy).
+// Planes [xbeg, xbeg + gridDim.z) of the slab.
+template <typename T, int BC, bool IMPORT>
 __global__ void __launch_bounds__(256) k0_init_pull(const double* __restrict__ rho, const double* __restrict__ u,
-                                                   T* __restrict__ A, StepParams<T> P) {
+                                                   const double* __restrict__ src, long long cstride,
+                                                   T* __restrict__ A, StepParams<T> P, int xbeg, int wx0) {
     const int z = blockIdx.x * 32 + threadIdx.x;
     const int y = blockIdx.y * 8 + threadIdx.y;
-    const int x = blockIdx.z;
+    const int x = xbeg + int(blockIdx.z);
     const SlabGeom& g = P.g;
     if (z >= g.nz || y >= g.ny) return;
-    auto cell_of = [&](int xx, int yy, int zz) { return ((long long)xx * g.ny + yy) * g.nz + zz; };
-    T r, ux, uy, uz;
-    k0_load<T>(rho, u, cell_of(x, y, z), r, ux, uy, uz);
+    const long long own = k0_wcell(g, wx0, x, y, z);
     T feq[kQ];
-    equilibrium<T>(r, ux, uy, uz, feq);  // own cell: slot 0 and the wall links
+    if constexpr (!IMPORT) {
+        T r, ux, uy, uz;
+        k0_load<T>(rho, u, own, r, ux, uy, uz);
+        equilibrium<T>(r, ux, uy, uz, feq);  // own cell: slot 0 and the wall links
+    }
     const long long self = cell_off(g, x, y, z);
     static_for<0, kQ>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
@@ -166,7 +220,8 @@ __global__ void __launch_bounds__(256) k0_init_pull(const double* __restrict__ r
         constexpr int cx = can_cx(j), cy = can_cy(j), cz = can_cz(j);
         T v;
         if constexpr (j == 0) {
-            v = feq[0];
+            if constexpr (IMPORT) v = T(src[own]);
+            else v = feq[0];
         } else {
             int tx = x + cx, ty = y + cy, tz = z + cz;
             bool wall = false;
@@ -186,12 +241,18 @@ __global__ void __launch_bounds__(256) k0_init_pull(const double* __restrict__ r
                 if constexpr (cz == 1) tz = z == g.nz - 1 ? 0 : tz;
             }
             if (!wall) {
-                T rn, uxn, uyn, uzn;
-                k0_load<T>(rho, u, cell_of(tx, ty, tz), rn, uxn, uyn, uzn);
-                v = feq_dir<T, j>(rn, uxn, uyn, uzn);
+                const long long t = k0_wcell(g, wx0, tx, ty, tz);
+                if constexpr (IMPORT) {
+                    v = T(src[(long long)j * cstride + t]);
+                } else {
+                    T rn, uxn, uyn, uzn;
+                    k0_load<T>(rho, u, t, rn, uxn, uyn, uzn);
+                    v = feq_dir<T, j>(rn, uxn, uyn, uzn);
+                }
             } else {
                 constexpr int ko = slot_opp(k);
-                v = feq[can_opp(j)];
+                if constexpr (IMPORT) v = T(src[(long long)can_opp(j) * cstride + own]);
+                else v = feq[can_opp(j)];
                 if constexpr (cz == 1) {
                     if (z == g.nz - 1) v = v - P.lid[ko];
                 }
@@ -274,6 +335,21 @@ cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
 }
 
 template <typename T>
+cudaError_t launch_k1_sc(T* F, const StepParams<T>& P, int out_poff, unsigned* sync, cudaStream_t s) {
+    const SlabGeom& g = P.g;
+    if (g.nxl <= 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(sync, 0, sizeof(unsigned) * (1 + g.nxl), s);
+    if (e != cudaSuccess) return e;
+    const int tiles_z = (g.nz + 31) / 32, tpp = tiles_z * ((g.ny + 7) / 8);
+    const unsigned grid = unsigned((long long)tpp * g.nxl);
+    if (g.bc == BC_PERIODIC)
+        k1_step_sc<T, BC_PERIODIC><<<grid, kBlock, 0, s>>>(F, P, out_poff, sync, tiles_z, tpp);
+    else
+        k1_step_sc<T, BC_CAVITY><<<grid, kBlock, 0, s>>>(F, P, out_poff, sync, tiles_z, tpp);
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, const SlabGeom& g, cudaStream_t s,
                                   int xbeg, int nxc) {
     if (nxc < 0) nxc = g.nxl;
@@ -283,12 +359,21 @@ cudaError_t launch_k0_equilibrium(const double* rho, const double* u, T* C, cons
 }
 
 template <typename T>
-cudaError_t launch_k0_init_pull(const double* rho, const double* u, T* A, const StepParams<T>& P, cudaStream_t s) {
+cudaError_t launch_k0_init_pull(const double* rho, const double* u, const double* src, T* A, const StepParams<T>& P,
+                                int xbeg, int nxc, int wx0, int wn, cudaStream_t s) {
     const SlabGeom& g = P.g;
-    if (g.bc == BC_PERIODIC)
-        k0_init_pull<T, BC_PERIODIC><<<cell_grid(g.nz, g.ny, g.nxl), kBlock, 0, s>>>(rho, u, A, P);
-    else
-        k0_init_pull<T, BC_CAVITY><<<cell_grid(g.nz, g.ny, g.nxl), kBlock, 0, s>>>(rho, u, A, P);
+    if (nxc <= 0) return cudaSuccess;
+    const long long cstride = (long long)wn * g.ny * g.nz;
+    const dim3 grid = cell_grid(g.nz, g.ny, nxc);
+#define LBM_K0P(BC, IMP) k0_init_pull<T, BC, IMP><<<grid, kBlock, 0, s>>>(rho, u, src, cstride, A, P, xbeg, wx0)
+    if (g.bc == BC_PERIODIC) {
+        if (src) LBM_K0P(BC_PERIODIC, true);
+        else LBM_K0P(BC_PERIODIC, false);
+    } else {
+        if (src) LBM_K0P(BC_CAVITY, true);
+        else LBM_K0P(BC_CAVITY, false);
+    }
+#undef LBM_K0P
     return cudaGetLastError();
 }
 
@@ -329,11 +414,12 @@ cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int 
 
 #define LBM_INSTANTIATE(T)                                                                                   \
     template cudaError_t launch_k1<T>(const T*, T*, const StepParams<T>&, int, int, cudaStream_t);           \
+    template cudaError_t launch_k1_sc<T>(T*, const StepParams<T>&, int, unsigned*, cudaStream_t);            \
     template cudaError_t launch_k0_equilibrium<T>(const double*, const double*, T*, const SlabGeom&,         \
                                                   cudaStream_t, int, int);                                   \
     template cudaError_t launch_k0_unstream<T>(const T*, T*, const StepParams<T>&, cudaStream_t);            \
-    template cudaError_t launch_k0_init_pull<T>(const double*, const double*, T*, const StepParams<T>&,      \
-                                                cudaStream_t);                                               \
+    template cudaError_t launch_k0_init_pull<T>(const double*, const double*, const double*, T*,             \
+                                                const StepParams<T>&, int, int, int, int, cudaStream_t);     \
     template cudaError_t launch_k0_import<T>(const double*, T*, const SlabGeom&, int, int, cudaStream_t);    \
     template cudaError_t launch_k3_materialize<T>(const T*, const StepParams<T>&, int, int, int, int, int,   \
                                                   int, double*, cudaStream_t);                               \

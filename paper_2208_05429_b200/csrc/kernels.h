@@ -10,10 +10,25 @@ namespace lbm {
 template <typename T>
 cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s);
 
-// K2: two fused steps, A = f*(t-1) -> B = f*(t+1) on planes [xbeg, xbeg+nxs).
-// A's two ghost planes per side must be valid.
+// K1 in place on single-copy ring storage: output plane x to ring slot
+// x + 2 + out_poff (= the slot of input plane x - 4); sync = device scratch
+// of nxl + 1 words.
 template <typename T>
-cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s);
+cudaError_t launch_k1_sc(T* F, const StepParams<T>& P, int out_poff, unsigned* sync, cudaStream_t s);
+constexpr int kK1ScGap = 4;
+
+// K2: two fused steps, A = f*(t-1) -> B = f*(t+1) on planes [xbeg, xbeg+nxs).
+// A's two ghost planes per side must be valid.  Output plane d goes to ring
+// slot d + 2 + out_poff (mod P.g.pmod).  Single-copy ring storage: B == A,
+// out_poff = P.g.poff - k2_sc_gap (mod pmod), and sc_sync = device scratch of
+// k2_sc_max_chunks(nxl) + 1 words (the chunk-ordered tickets).
+template <typename T>
+cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s, int out_poff = 0,
+                      unsigned* sc_sync = nullptr);
+template <typename T>
+int k2_sc_gap();
+template <typename T>
+int k2_sc_max_chunks(int nxl);
 template <typename T>
 bool k2_supported(const SlabGeom& g);
 // K2R: the same two-step sweep with register-staged gathers and two warp
@@ -41,9 +56,13 @@ cudaError_t launch_aa_merge(T* dst, const T* src, const SlabGeom& g, int slot0, 
 template <typename T>
 cudaError_t launch_aa_moments(const T* F, const StepParams<T>& P, bool odd, int xbeg, int nxc, double* rho,
                               double* u, cudaStream_t s);
-// K0 fused, one slab spanning the domain: the pull-form state from rho, u
+// K0 fused, one slab spanning the domain: the pull-form state of planes
+// [xbeg, xbeg + nxc) from rho, u (src == null) or from canonical doubles
+// src[19][wn][ny][nz]; the per-cell inputs hold the wn planes wx0, wx0 + 1,
+// ... (mod nxl), which must include the planes' x neighbours.
 template <typename T>
-cudaError_t launch_k0_init_pull(const double* rho, const double* u, T* A, const StepParams<T>& P, cudaStream_t s);
+cudaError_t launch_k0_init_pull(const double* rho, const double* u, const double* src, T* A, const StepParams<T>& P,
+                                int xbeg, int nxc, int wx0, int wn, cudaStream_t s);
 template <typename T>
 cudaError_t launch_k0_unstream(const T* C, T* A, const StepParams<T>& P, cudaStream_t s);
 template <typename T>

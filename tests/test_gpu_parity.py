@@ -416,18 +416,20 @@ def _sample_boxes(cfg):
     return [(o, sz) for o in cand]
 
 
-@pytest.mark.parametrize("cfg_id,dtype", [(3, "f64"), (4, "f64"), (5, "f64"), (5, "f32")])
-def test_full_size_sampled_parity(cfg_id, dtype):
+@pytest.mark.parametrize("cfg_id,dtype,kernel", [(3, "f64", 0), (4, "f64", 0), (5, "f64", 0), (5, "f32", 0),
+                                                 (5, "f64", lbm.LBM_KERNEL_K2_SC), (3, "f32", lbm.LBM_KERNEL_K2_SC)])
+def test_full_size_sampled_parity(cfg_id, dtype, kernel):
     """BASELINE.json configs 3-5 at their FULL sizes, in the launch
-    configuration bench.py times (K2 sweeps, x-chunks, 1 GPU): sampled boxes
-    of the GPU state equal the oracle's sub-box steps (oracle.step_box, the
-    core away from unknown pulls) after one two-step sweep and one more
-    single step; the mass of the cavities is conserved over the domain."""
+    configuration bench.py times (K2 sweeps, x-chunks, 1 GPU; and the
+    single-copy ring, K2_SC): sampled boxes of the GPU state equal the
+    oracle's sub-box steps (oracle.step_box, the core away from unknown
+    pulls) after one two-step sweep and one more single step; the mass of the
+    cavities is conserved over the domain."""
     cfg = li.CONFIGS[cfg_id]
     rho, u = li.init_fields(cfg)
     boxes = _sample_boxes(cfg)
     dims = (cfg.nx, cfg.ny, cfg.nz)
-    with lbm.Lattice(*dims, cfg.tau, cfg.u_lid, dtype, bc=cfg.bc) as lat:
+    with lbm.Lattice(*dims, cfg.tau, cfg.u_lid, dtype, bc=cfg.bc, kernel=kernel) as lat:
         lat.init_equilibrium(rho, u)
         r0, _ = lat.macroscopic()
         m0 = float(np.sum(r0, dtype=np.float64))
