@@ -69,6 +69,27 @@ def test_create_rejects_bad_partitions():
         lbm.lbm_create_ex(1, 4, 4, 0.6, None, "f64", o)
 
 
+def test_create_rejects_bad_kernel_choices():
+    o = lbm.lbm_default_opts()
+    o.kernel = 6
+    with pytest.raises(lbm.LbmError, match="bad kernel"):
+        lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+    o.kernel, o.comm, o.local_slabs = lbm.LBM_KERNEL_K2_SC, lbm.LBM_COMM_LOCAL, 2
+    with pytest.raises(lbm.LbmError, match="K2_SC needs a single slab"):
+        lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+
+
+def test_header_enums_match_binding():
+    """Every enumerator of include/lbm.h has the same value in the binding."""
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "lbm.h")).read(), flags=re.S)
+    found = 0
+    for body in re.findall(r"typedef enum\s*\{(.*?)\}", src, flags=re.S):
+        for name, val in re.findall(r"\b(LBM_[A-Z0-9_]+)\s*=\s*(\d+)", body):
+            assert getattr(lbm, name) == int(val), name
+            found += 1
+    assert found >= 17
+
+
 def test_step_rejects_negative_and_null():
     with pytest.raises(lbm.LbmError):
         lbm.lbm_step(None, 1)
