@@ -104,6 +104,7 @@ struct lbm_ctx {
     bool sc = false;
     int sc_gap = 0;
     unsigned* sc_sync = nullptr;
+    bool fused_halo = true;  // K2 stores the neighbours' ghost planes itself (run_steps)
     ncclComm_t comm = nullptr;
     size_t esize = 8;
     int* d_flag = nullptr;
@@ -476,14 +477,22 @@ lbm_status run_steps(lbm_ctx* c, long n) {
         for (const Slab& s : c->slabs) use_k2 = use_k2 && k2r_supported<T>(s.g);
     if (c->opts.kernel >= LBM_KERNEL_K2 && !use_k2 && n >= 2)
         return fail(c, LBM_EINVAL, "two-step kernel requested but not supported for this geometry");
+    // Fused halo (k2.cu): TMA K2 sweeps store the neighbours' ghost planes
+    // themselves when the neighbours' buffers are addressable here (one
+    // device: LOCAL slabs, the periodic self-wrap), so after the first sweep
+    // no exchange runs.  LBM_FUSED_HALO=0 turns it off (A/B runs, tests).
+    const bool fuse = tma && c->fused_halo && c->opts.comm != LBM_COMM_NCCL;
     while (n > 0) {
         const int nsteps = (use_k2 && n >= 2) ? 2 : 1;
+        const bool fused = fuse && nsteps == 2;
         auto launch = [&](Slab& s, int xbeg, int nxs) -> cudaError_t {
             const StepParams<T> P = make_params<T>(c, s);
             const T* A = static_cast<const T*>(s.buf[c->cur]);
             T* B = static_cast<T*>(s.buf[c->cur ^ 1]);
+            T* hl = fused && s.left >= 0 ? static_cast<T*>(c->slabs[s.left].buf[c->cur ^ 1]) : nullptr;
+            T* hr = fused && s.right >= 0 ? static_cast<T*>(c->slabs[s.right].buf[c->cur ^ 1]) : nullptr;
             return nsteps == 1 ? launch_k1<T>(A, B, P, xbeg, nxs, c->stream)
-                   : tma       ? launch_k2<T>(A, B, P, xbeg, nxs, c->stream)
+                   : tma       ? launch_k2<T>(A, B, P, xbeg, nxs, c->stream, 0, nullptr, hl, hr)
                                : launch_k2r<T>(A, B, P, xbeg, nxs, c->stream);
         };
         // Planes [h, nxl-h) read no ghost plane (h = the sweep's step count),
@@ -527,7 +536,7 @@ lbm_status run_steps(lbm_ctx* c, long n) {
         if (pst != LBM_OK) return pst;
         (nsteps == 2 ? c->k2_launches : c->k1_launches) += (long long)c->slabs.size();
         c->cur ^= 1;
-        c->ghosts_valid = false;
+        c->ghosts_valid = fused;
         c->t += nsteps;
         n -= nsteps;
     }
@@ -1112,6 +1121,8 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         // so there it is off.  LBM_OVERLAP=0/1 forces it (A/B runs, tests).
         const char* e = getenv("LBM_OVERLAP");
         c->overlap = e ? e[0] == '1' : o.comm == LBM_COMM_NCCL;
+        const char* f = getenv("LBM_FUSED_HALO");
+        c->fused_halo = !(f && f[0] == '0');
     }
     if (o.comm == LBM_COMM_NCCL) {
         if (!nccl_load()) return bail(fail(c, LBM_ENCCL, "cannot load libnccl.so.2"));

@@ -147,7 +147,7 @@ __device__ __forceinline__ int wrapi(int v, int n) {
 template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
 __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     k2_sweep(const __grid_constant__ CUtensorMap tmA, const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
-             int xbeg, int xend, int chunk, int out_poff, unsigned* __restrict__ sc_sync) {
+             int xbeg, int xend, int chunk, int out_poff, unsigned* __restrict__ sc_sync, T* haloL, T* haloR) {
     using C = K2Cfg<T, TY, TZ>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* const stage = reinterpret_cast<T*>(smem_raw);
@@ -464,6 +464,29 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 constexpr int k = decltype(kc)::value;
                 __stcs(Bd + (long long)k * g.pq + st_off, f2[slot_dir(k)]);
             });
+            if constexpr (!RING) {
+                // Fused halo: the planes a neighbouring
+                // slab reads as ghosts also go straight into its next-sweep
+                // buffer -- planes 0 (all slots) and 1 (c_x = -1 slots) into
+                // the left neighbour's x = nxl, nxl+1; planes nxl-2 (c_x = +1
+                // slots) and nxl-1 (all) into the right neighbour's x = -2, -1
+                // (the halo plan's spans, fill_plan) -- instead of a separate
+                // exchange after the sweep.
+                if (d <= 1 && haloL) {
+                    T* const H = haloL + (long long)(g.nxl + 2 + d) * g.px;
+                    static_for<0, kQ>([&](auto kc) {
+                        constexpr int k = decltype(kc)::value;
+                        if (d == 0 || k < kSlotsM) __stcs(H + (long long)k * g.pq + st_off, f2[slot_dir(k)]);
+                    });
+                }
+                if (d >= g.nxl - 2 && haloR) {
+                    T* const H = haloR + (long long)(d - g.nxl + 2) * g.px;
+                    static_for<0, kQ>([&](auto kc) {
+                        constexpr int k = decltype(kc)::value;
+                        if (d == g.nxl - 1 || k >= kSlotP0) __stcs(H + (long long)k * g.pq + st_off, f2[slot_dir(k)]);
+                    });
+                }
+            }
         }
         // ---------------- step 1: plane p (pushes) ----------------
         T* const wM = ringM + ((p + 1) & 1) * 5 * C::RP;  // dest p-1 (p + 1 has the parity of p - 1)
@@ -591,7 +614,7 @@ constexpr int k2_max_chunk() {
 
 template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
 cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, int out_poff,
-                           unsigned* sc_sync, cudaStream_t s) {
+                           unsigned* sc_sync, T* haloL, T* haloR, cudaStream_t s) {
     using C = K2Cfg<T, TY, TZ>;
     constexpr int NT = C::NT;
     auto kern = k2_sweep<T, BC, TY, TZ, EARLY, RING>;
@@ -665,7 +688,7 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
         cudaError_t e = cudaMemsetAsync(sc_sync, 0, sizeof(unsigned) * (1 + grid.y), s);
         if (e != cudaSuccess) return e;
     }
-    kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk, out_poff, sc_sync);
+    kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk, out_poff, sc_sync, haloL, haloR);
     return cudaGetLastError();
 }
 
@@ -696,7 +719,7 @@ int k2_sc_max_chunks(int nxl) {
 
 template <typename T>
 cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s, int out_poff,
-                      unsigned* sc_sync) {
+                      unsigned* sc_sync, T* halo_left, T* halo_right) {
     if (nxs <= 0) return cudaSuccess;
     const bool per = P.g.bc == BC_PERIODIC;
     // Default: read the stage into registers and issue the next TMA before
@@ -710,16 +733,16 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
     }();
     if (sc_sync) {  // single-copy ring storage: the default shape only
         constexpr int TY = sizeof(T) == 8 ? 8 : 16, TZ = 32;
-        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, true>(A, B, P, xbeg, nxs, out_poff, sc_sync, s)
-                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, true>(A, B, P, xbeg, nxs, out_poff, sc_sync, s);
+        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, true>(A, B, P, xbeg, nxs, out_poff, sc_sync, nullptr, nullptr, s)
+                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, true>(A, B, P, xbeg, nxs, out_poff, sc_sync, nullptr, nullptr, s);
     }
 #define LBM_K2_TILE_CASE(TY, TZ)                                                                              \
     if constexpr (K2Cfg<T, TY, TZ>::FITS) {                                                                   \
         if (early)                                                                                            \
-            return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, s) \
-                       : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, s);  \
-        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, s)    \
-                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, s);     \
+            return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s) \
+                       : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s);  \
+        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s)    \
+                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s);     \
     } else {                                                                                                  \
         return cudaErrorInvalidConfiguration;                                                                 \
     }
@@ -741,9 +764,9 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
 template bool k2_supported<double>(const SlabGeom&);
 template bool k2_supported<float>(const SlabGeom&);
 template cudaError_t launch_k2<double>(const double*, double*, const StepParams<double>&, int, int, cudaStream_t,
-                                       int, unsigned*);
+                                       int, unsigned*, double*, double*);
 template cudaError_t launch_k2<float>(const float*, float*, const StepParams<float>&, int, int, cudaStream_t, int,
-                                      unsigned*);
+                                      unsigned*, float*, float*);
 template int k2_sc_gap<double>();
 template int k2_sc_gap<float>();
 template int k2_sc_max_chunks<double>(int);

@@ -219,12 +219,15 @@ K2_VARIANTS = [("LBM_K2R_CFG", v, 3) for v in ["8x32s0", "8x32s1", "8x16s0m2", "
     [("LBM_K2_TILE", v, 2) for v in ["8x32", "8x16", "16x16"]] + [("LBM_K2_EARLY", "0", 2), ("LBM_K2_CHUNK", "3", 2)]
 
 
+@pytest.mark.parametrize("fused", ["0", "1"])
 @pytest.mark.parametrize("overlap", ["0", "1"])
-def test_overlapped_exchange_bitwise(overlap, tmp_path):
+def test_overlapped_exchange_bitwise(overlap, fused, tmp_path):
     """The halo exchange overlapped with the interior sweep (comm stream +
-    interior/edge split, the NCCL default) and the serial exchange give the
-    bits of a single slab, for LOCAL slabs on one device and the periodic
-    self-wrap, K2 and K1 (odd step) sweeps, both dtypes."""
+    interior/edge split, the NCCL default), the serial exchange, and the
+    fused halo (K2 storing the neighbours' ghost planes itself, no exchange
+    after the first sweep) all give the bits of a single-slab K1 run, for
+    LOCAL slabs on one device and the periodic self-wrap, K2 and K1 (odd
+    step) sweeps, both dtypes, with read-backs between sweeps."""
     import subprocess
     import sys
     import os
@@ -235,14 +238,17 @@ def test_overlapped_exchange_bitwise(overlap, tmp_path):
         "  for dims, slabs in [((48, 12, 40), 4), ((24, 9, 33), 2), ((12, 8, 32), 1), ((16, 8, 32), 4)]:\n"
         "    for dt in ('f64', 'f32'):\n"
         "      f0 = li.random_populations(43, *dims); r = []\n"
-        "      for s in (1, slabs):\n"
+        "      for s, k in ((1, lbm.LBM_KERNEL_K1), (slabs, lbm.LBM_KERNEL_AUTO)):\n"
         "        kw = dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=s) if s > 1 else {}\n"
-        "        with lbm.Lattice(*dims, 0.6, (0.05, 0, 0), dt, bc=bc, **kw) as lat:\n"
-        "          lat.set_populations(f0); lat.step(3); lat.step(2); r.append(lat.populations())\n"
-        "      assert np.array_equal(r[0], r[1]), (bc, dims, dt)\n"
+        "        with lbm.Lattice(*dims, 0.6, (0.05, 0, 0), dt, bc=bc, kernel=k, **kw) as lat:\n"
+        "          lat.set_populations(f0); out = []\n"
+        "          for n in (3, 2, 4, 2):\n"
+        "            lat.step(n); out.append(lat.populations()); out.extend(lat.macroscopic())\n"
+        "          r.append(out)\n"
+        "      for a, b in zip(*r): assert np.array_equal(a, b), (bc, dims, dt)\n"
         "print('ok')\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PYTHONPATH=root, LBM_OVERLAP=overlap)
+    env = dict(os.environ, PYTHONPATH=root, LBM_OVERLAP=overlap, LBM_FUSED_HALO=fused)
     out = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
 

@@ -7,6 +7,7 @@ Variant shapes are selected by the env vars LBM_K2R_CFG / LBM_K2_TILE."""
 import argparse
 import os
 import statistics
+import time
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -55,14 +56,16 @@ with lbm.Lattice(nx, ny, nz, 0.6, (0.05, 0, 0), a.dtype, bc=bc, kernel=kern, **k
     for _ in range(a.reps):
         lbm.lbm_profile_enable(lat.ctx, True)
         lbm.lbm_profile_reset(lat.ctx)
+        t0 = time.perf_counter()
         lat.step(a.steps)
         lbm.lbm_synchronize(lat.ctx)
+        wall = time.perf_counter() - t0  # whole steps: sweeps + halo exchanges + launch gaps
         st = lbm.lbm_get_stats(lat.ctx)
         lbm.lbm_profile_enable(lat.ctx, False)
         ms = st.sweep_ms / max(1, st.sweep_launches)  # one record per sweep of all slabs
         steps_per = st.sweep_updates / max(1, st.sweep_launches) / (nx * ny * nz)
         mlups = nx * ny * nz * steps_per / (ms * 1e-3) / 1e6
-        res.append((mlups, ms))
+        res.append((mlups, ms, nx * ny * nz * a.steps / wall / 1e6))
     if samp is not None:
         stop.set()
         th.join()
@@ -73,5 +76,6 @@ with lbm.Lattice(nx, ny, nz, 0.6, (0.05, 0, 0), a.dtype, bc=bc, kernel=kern, **k
     med = statistics.median(r[0] for r in res)
     gbs = best * 1e6 * 19 * es * (2 / steps_per) / 1e9
     print(f"{a.tag or a.kernel:24s} {a.dtype} {a.dims:14s} best {best:9.1f} MLUPS  median {med:9.1f}  "
-          f"sweep {min(r[1] for r in res):8.3f} ms  algorithmic {gbs:7.1f} GB/s"
+          f"sweep {min(r[1] for r in res):8.3f} ms  algorithmic {gbs:7.1f} GB/s  "
+          f"whole-step {max(r[2] for r in res):9.1f} MLUPS"
           + (f"  sm {clk:.0f} MHz  {pw:.0f} W" if samp is not None else ""), flush=True)
