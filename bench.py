@@ -291,7 +291,8 @@ def main():
     sweep_updates = s1.sweep_updates
     k2 = s1.k2_launches - s0.k2_launches
     k1 = s1.k1_launches - s0.k1_launches
-    dominant = "k2_two_step" if k2 >= k1 else ("aa_step" if args.kernel == "aa" else "k1_step")
+    dominant = (("k2_single_copy" if args.kernel == "k2sc" else "k2_two_step") if k2 >= k1
+                else ("aa_step" if args.kernel == "aa" else "k1_step"))
     # per launch: cells_local x 2 x 19 x es bytes (both K1 and K2 stream the lattice once)
     bytes_per_launch = cells_local * 2 * 19 * es
     avg_launch_ms = sweep_ms / max(1, sweep_launches)

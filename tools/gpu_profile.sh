@@ -6,6 +6,9 @@ for dt in f64 f32; do
   $CMD > gpurun_out/plain_$dt.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:k2_sweep -s 2 -c 1 -o gpurun_out/r01_k2_${dt}_cfg5 $CMD > gpurun_out/ncu_k2_$dt.log 2>&1
 done
+CMD="python tools/sweep_bench.py --dims 1024,512,512 --steps 2 --reps 1 --kernel k2sc --dtype f64"
+$CMD > gpurun_out/plain_k2sc.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k2_sweep -s 2 -c 1 -o gpurun_out/r01_k2sc_f64_cfg5 $CMD > gpurun_out/ncu_k2sc.log 2>&1
 CMD="python tools/sweep_bench.py --dims 1024,512,512 --steps 2 --reps 1 --kernel k1 --dtype f64"
 $CMD > gpurun_out/plain_k1.log 2>&1 && \
 ncu --set full --clock-control none -k regex:k1_step -s 4 -c 1 -o gpurun_out/r01_k1_f64_cfg5 $CMD > gpurun_out/ncu_k1.log 2>&1
