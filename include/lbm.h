@@ -69,7 +69,11 @@ typedef enum {
     LBM_ENOMEM = 2,
     LBM_ECUDA = 3,
     LBM_ENCCL = 4,
-    LBM_ESTATE = 5
+    LBM_ESTATE = 5,
+    /* lbm_macroscopic found rho == 0 (degenerate moments: never
+     * a silent division) or non-finite moments (a diverged state) in some
+     * cell; the outputs are written, the context stays usable. */
+    LBM_ENUMERIC = 6
 } lbm_status;
 
 /* Sweep kernel selection.  K1: one fused collide+stream step per HBM pass
@@ -165,9 +169,11 @@ lbm_status lbm_step(lbm_ctx *ctx, long n);
 /* Moments of the canonical f(t): rho = sum_i f_i, u = (sum_i c_i f_i)/rho
  * (the paper's velocity norms).  Host arrays
  * rho [nx_local][ny][nz], u [nx_local][ny][nz][3]; either may be NULL.
- * Blocks until the copy is complete. */
+ * Blocks until the copy is complete.  ENUMERIC if some cell has rho == 0 or
+ * non-finite moments (the arrays are still filled). */
 lbm_status lbm_macroscopic(lbm_ctx *ctx, double *rho, double *u);
-/* Same into DEVICE arrays; asynchronous on the context stream. */
+/* Same into DEVICE arrays; asynchronous on the context stream (no ENUMERIC
+ * check: it would need a synchronisation). */
 lbm_status lbm_macroscopic_device(lbm_ctx *ctx, double *d_rho, double *d_u);
 
 /* Canonical populations f(t) as host f[19][nx_local][ny][nz] (canonical

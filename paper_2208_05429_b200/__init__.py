@@ -29,8 +29,9 @@ LBM_F64, LBM_F32 = 0, 1
 LBM_BC_CAVITY, LBM_BC_PERIODIC = 0, 1
 LBM_KERNEL_AUTO, LBM_KERNEL_K1, LBM_KERNEL_K2, LBM_KERNEL_K2_REG, LBM_KERNEL_AA, LBM_KERNEL_K2_SC = 0, 1, 2, 3, 4, 5
 LBM_COMM_NONE, LBM_COMM_NCCL, LBM_COMM_LOCAL = 0, 1, 2
-LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_ESTATE = 0, 1, 2, 3, 4, 5
-STATUS = {0: "LBM_OK", 1: "LBM_EINVAL", 2: "LBM_ENOMEM", 3: "LBM_ECUDA", 4: "LBM_ENCCL", 5: "LBM_ESTATE"}
+LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_ESTATE, LBM_ENUMERIC = 0, 1, 2, 3, 4, 5, 6
+STATUS = {0: "LBM_OK", 1: "LBM_EINVAL", 2: "LBM_ENOMEM", 3: "LBM_ECUDA", 4: "LBM_ENCCL", 5: "LBM_ESTATE",
+          6: "LBM_ENUMERIC"}
 DTYPES = {"f64": LBM_F64, "float64": LBM_F64, "fp64": LBM_F64, "f32": LBM_F32, "float32": LBM_F32, "fp32": LBM_F32}
 
 

@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(256) k_aa_materialize(const T* __restrict__ F,
 
 template <typename T, int BC>
 __global__ void __launch_bounds__(256) k_aa_moments(const T* __restrict__ F, StepParams<T> P, int odd, int xbeg,
-                                                   int nxc, double* __restrict__ rho, double* __restrict__ u) {
+                                                   int nxc, double* __restrict__ rho, double* __restrict__ u,
+                                                   int* flag) {
     const int z = blockIdx.x * 32 + threadIdx.x;
     const int y = blockIdx.y * 8 + threadIdx.y;
     const int xc = blockIdx.z;
@@ -170,6 +171,10 @@ __global__ void __launch_bounds__(256) k_aa_moments(const T* __restrict__ F, Ste
     aa_gather<T, BC>(F, P, odd != 0, xbeg + xc, y, z, f);
     T r, ux, uy, uz;
     moments<T>(f, r, ux, uy, uz);
+    if (flag) {
+        const int bad = moments_flags<T>(r, ux, uy, uz);
+        if (bad) atomicOr(flag, bad);
+    }
     const long long cell = ((long long)xc * P.g.ny + y) * P.g.nz + z;
     if (rho) rho[cell] = double(r);
     if (u) {
@@ -240,12 +245,12 @@ cudaError_t launch_aa_materialize(const T* F, const StepParams<T>& P, bool odd, 
 
 template <typename T>
 cudaError_t launch_aa_moments(const T* F, const StepParams<T>& P, bool odd, int xbeg, int nxc, double* rho,
-                              double* u, cudaStream_t s) {
+                              double* u, cudaStream_t s, int* flag) {
     const dim3 grid = aa_grid(P.g.nz, P.g.ny, nxc);
     if (P.g.bc == BC_PERIODIC)
-        k_aa_moments<T, BC_PERIODIC><<<grid, kAABlock, 0, s>>>(F, P, odd, xbeg, nxc, rho, u);
+        k_aa_moments<T, BC_PERIODIC><<<grid, kAABlock, 0, s>>>(F, P, odd, xbeg, nxc, rho, u, flag);
     else
-        k_aa_moments<T, BC_CAVITY><<<grid, kAABlock, 0, s>>>(F, P, odd, xbeg, nxc, rho, u);
+        k_aa_moments<T, BC_CAVITY><<<grid, kAABlock, 0, s>>>(F, P, odd, xbeg, nxc, rho, u, flag);
     return cudaGetLastError();
 }
 
@@ -254,7 +259,7 @@ cudaError_t launch_aa_moments(const T* F, const StepParams<T>& P, bool odd, int 
     template cudaError_t launch_aa_materialize<T>(const T*, const StepParams<T>&, bool, int, int, int, int,   \
                                                   int, int, double*, cudaStream_t);                          \
     template cudaError_t launch_aa_moments<T>(const T*, const StepParams<T>&, bool, int, int, double*,       \
-                                              double*, cudaStream_t);                                        \
+                                              double*, cudaStream_t, int*);                                  \
     template cudaError_t launch_aa_merge<T>(T*, const T*, const SlabGeom&, int, cudaStream_t);
 LBM_AA_INSTANTIATE(double)
 LBM_AA_INSTANTIATE(float)

@@ -822,10 +822,25 @@ lbm_status set_pops(lbm_ctx* c, const double* f) {
     return finish_init<T>(c, canon);
 }
 
+// After a blocking read-back: the moments flags (moments_flags, d3q19.cuh)
+// as a status -- an explicit error for rho == 0, never a silent division
+// (SPEC.md:68), and for a diverged (non-finite) state.  The outputs are
+// written either way; the context stays usable.
+lbm_status moments_status(lbm_ctx* c) {
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (flag & 1) return fail(c, LBM_ENUMERIC, "degenerate moments: rho == 0 in some cell (u undefined there)");
+    if (flag & 2) return fail(c, LBM_ENUMERIC, "non-finite moments: the state has diverged");
+    return LBM_OK;
+}
+
 template <typename T>
 lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
     lbm_status st = ensure_ghosts(c);
     if (st != LBM_OK) return st;
+    int* const flag = host ? c->d_flag : nullptr;  // the blocking read-back checks the moments
+    if (flag) CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
     const long long plane = (long long)c->ny * c->nz;
     const int cap = int(std::max<long long>(1, (long long)(c->stage_bytes / (4 * sizeof(double))) / plane));
     double* stage = static_cast<double*>(c->stage);
@@ -834,8 +849,8 @@ lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
         const T* F = static_cast<const T*>(s.buf[0]);
         // AA: the phase-aware moments; single-copy ring: K3 on the window
         auto moments = [&](int xb, int nxc, double* r, double* v) {
-            return c->sc ? launch_k3_moments<T>(F, P, xb, nxc, r, v, c->stream)
-                         : launch_aa_moments<T>(F, P, c->aa_odd, xb, nxc, r, v, c->stream);
+            return c->sc ? launch_k3_moments<T>(F, P, xb, nxc, r, v, c->stream, flag)
+                         : launch_aa_moments<T>(F, P, c->aa_odd, xb, nxc, r, v, c->stream, flag);
         };
         const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;
         if (!host) {
@@ -856,8 +871,7 @@ lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
                                    c->stream));
         }
     }
-    if (host) CK(cudaStreamSynchronize(c->stream));
-    return LBM_OK;
+    return host ? moments_status(c) : LBM_OK;
 }
 
 template <typename T>
@@ -865,6 +879,8 @@ lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
     if (c->aa || c->sc) return macro_aa<T>(c, rho, u, host);
     lbm_status st = ensure_ghosts(c);
     if (st != LBM_OK) return st;
+    int* const flag = host ? c->d_flag : nullptr;  // the blocking read-back checks the moments
+    if (flag) CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
     const long long plane = (long long)c->ny * c->nz;
     for (Slab& s : c->slabs) {
         const StepParams<T> P = make_params<T>(c, s);
@@ -874,7 +890,7 @@ lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
         if (host) {
             double* stage = static_cast<double*>(s.buf[c->cur ^ 1]);
             CK(launch_k3_moments<T>(A, P, 0, s.g.nxl, rho ? stage : nullptr, u ? stage + cells : nullptr,
-                                    c->stream));
+                                    c->stream, flag));
             c->launches++;
             if (rho)
                 CK(cudaMemcpyAsync(rho + xoff, stage, cells * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -887,8 +903,7 @@ lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
             c->launches++;
         }
     }
-    if (host) CK(cudaStreamSynchronize(c->stream));
-    return LBM_OK;
+    return host ? moments_status(c) : LBM_OK;
 }
 
 // box in process-local coordinates; out f[19][lx][ly][lz]

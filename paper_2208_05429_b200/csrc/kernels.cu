@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(256) k3_materialize(const T* __restrict__ A, S
 // u[x][y][z][3] (doubles, chunk-local x).
 template <typename T, int BC>
 __global__ void __launch_bounds__(256) k3_moments(const T* __restrict__ A, StepParams<T> P, int xbeg, int nxc,
-                                                 double* __restrict__ rho, double* __restrict__ u) {
+                                                 double* __restrict__ rho, double* __restrict__ u, int* flag) {
     const int z = blockIdx.x * 32 + threadIdx.x;
     const int y = blockIdx.y * 8 + threadIdx.y;
     const int xc = blockIdx.z;
@@ -311,6 +311,10 @@ __global__ void __launch_bounds__(256) k3_moments(const T* __restrict__ A, StepP
     pull_cell<T, BC>(A, P, xbeg + xc, y, z, f);
     T r, ux, uy, uz;
     moments<T>(f, r, ux, uy, uz);
+    if (flag) {
+        const int bad = moments_flags<T>(r, ux, uy, uz);
+        if (bad) atomicOr(flag, bad);
+    }
     const long long cell = ((long long)xc * P.g.ny + y) * P.g.nz + z;
     if (rho) rho[cell] = double(r);
     if (u) {
@@ -404,11 +408,11 @@ cudaError_t launch_k3_materialize(const T* A, const StepParams<T>& P, int x0, in
 
 template <typename T>
 cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int nxc, double* rho, double* u,
-                              cudaStream_t s) {
+                              cudaStream_t s, int* flag) {
     if (P.g.bc == BC_PERIODIC)
-        k3_moments<T, BC_PERIODIC><<<cell_grid(P.g.nz, P.g.ny, nxc), kBlock, 0, s>>>(A, P, xbeg, nxc, rho, u);
+        k3_moments<T, BC_PERIODIC><<<cell_grid(P.g.nz, P.g.ny, nxc), kBlock, 0, s>>>(A, P, xbeg, nxc, rho, u, flag);
     else
-        k3_moments<T, BC_CAVITY><<<cell_grid(P.g.nz, P.g.ny, nxc), kBlock, 0, s>>>(A, P, xbeg, nxc, rho, u);
+        k3_moments<T, BC_CAVITY><<<cell_grid(P.g.nz, P.g.ny, nxc), kBlock, 0, s>>>(A, P, xbeg, nxc, rho, u, flag);
     return cudaGetLastError();
 }
 
@@ -424,7 +428,7 @@ cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int 
     template cudaError_t launch_k3_materialize<T>(const T*, const StepParams<T>&, int, int, int, int, int,   \
                                                   int, double*, cudaStream_t);                               \
     template cudaError_t launch_k3_moments<T>(const T*, const StepParams<T>&, int, int, double*, double*,    \
-                                              cudaStream_t);
+                                              cudaStream_t, int*);
 LBM_INSTANTIATE(double)
 LBM_INSTANTIATE(float)
 

@@ -58,7 +58,7 @@ template <typename T>
 cudaError_t launch_aa_merge(T* dst, const T* src, const SlabGeom& g, int slot0, cudaStream_t s);
 template <typename T>
 cudaError_t launch_aa_moments(const T* F, const StepParams<T>& P, bool odd, int xbeg, int nxc, double* rho,
-                              double* u, cudaStream_t s);
+                              double* u, cudaStream_t s, int* flag = nullptr);
 // K0 fused, one slab spanning the domain: the pull-form state of planes
 // [xbeg, xbeg + nxc) from rho, u (src == null) or from canonical doubles
 // src[19][wn][ny][nz]; the per-cell inputs hold the wn planes wx0, wx0 + 1,
@@ -73,8 +73,9 @@ cudaError_t launch_k0_import(const double* src, T* C, const SlabGeom& g, int xbe
 template <typename T>
 cudaError_t launch_k3_materialize(const T* A, const StepParams<T>& P, int x0, int y0, int z0, int lx, int ly,
                                   int lz, double* out, cudaStream_t s);
+// flag (nullable): |= moments_flags() of every cell (degenerate / non-finite)
 template <typename T>
 cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int nxc, double* rho, double* u,
-                              cudaStream_t s);
+                              cudaStream_t s, int* flag = nullptr);
 
 }  // namespace lbm

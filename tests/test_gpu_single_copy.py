@@ -151,3 +151,29 @@ def test_single_copy_randomised_bitwise():
                     lat.step(n)
                 res.append(lat.populations())
         assert np.array_equal(res[0], res[1]), (dims, bc, dtype, splits, tau)
+
+
+@pytest.mark.parametrize("kernel", [lbm.LBM_KERNEL_AUTO, lbm.LBM_KERNEL_AA, SC])
+def test_degenerate_and_diverged_moments_are_reported(kernel):
+    """lbm_macroscopic never divides silently: a cell whose
+    populations sum to zero gives LBM_ENUMERIC ("degenerate"), a state whose
+    moments overflow gives LBM_ENUMERIC ("non-finite"); the arrays are still
+    written and the context stays usable.  Every storage (K2 pull, AA, ring)."""
+    dims = (4, 6, 8)
+    f0 = li.random_populations(91, *dims)
+    f0[:, 2, 3, 4] = 0.0
+    with lbm.Lattice(*dims, 0.6, (0.0, 0.0, 0.0), "f64", bc=lbm.LBM_BC_PERIODIC, kernel=kernel) as lat:
+        lat.set_populations(f0)
+        with pytest.raises(lbm.LbmError, match="degenerate") as e:
+            lat.macroscopic()
+        assert e.value.status == lbm.LBM_ENUMERIC
+        assert np.array_equal(lat.populations(), f0)
+        f1 = li.random_populations(92, *dims)
+        lat.set_populations(f1)
+        rho, u = lat.macroscopic()
+        assert np.all(np.isfinite(u)) and np.allclose(rho, f1.sum(axis=0), rtol=1e-14)
+        f1[:, 1, 1, 1] = 1e308
+        lat.set_populations(f1)
+        with pytest.raises(lbm.LbmError, match="non-finite") as e:
+            lat.macroscopic()
+        assert e.value.status == lbm.LBM_ENUMERIC
