@@ -606,10 +606,12 @@ int num_sms() {
     return n;
 }
 
-// x chunks of at most k2_max_chunk planes (launch_k2_impl)
+// x chunks of at most k2_max_chunk planes (launch_k2_impl): fp64 56 on
+// large cross-sections (`wide`), else 32 -- the single-copy ring always 32,
+// which sets its gap (k2_sc_gap); fp32 48
 template <typename T>
-constexpr int k2_max_chunk() {
-    return sizeof(T) == 8 ? 32 : 48;
+constexpr int k2_max_chunk(bool wide = false) {
+    return sizeof(T) == 8 ? (wide ? 56 : 32) : 48;
 }
 
 template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
@@ -660,8 +662,15 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     // Among those, fill whole waves of the machine; each chunk re-computes
     // ~2.5 planes of step 1.
     // fp32 tiles (16x32) re-read relatively less x-halo per plane: 48 planes
-    // measured best there (65.9k -> 67.4k), 32 for fp64 (37.4k vs 36.9k)
-    constexpr int kMaxChunk = k2_max_chunk<T>();
+    // measured best there (65.9k -> 67.4k burst; 64 equal, 80 -4% in the
+    // sustained bench).  fp64: 32 planes at full clock (37.6k vs 35.8k at
+    // 56; 256^3 periodic 27.0k vs 26.2k), but a large lattice runs into the
+    // 1 kW power cap, and there the step-1 halo planes cost more than the
+    // L2 misses: sustained config 5 32.2k at 32, 32.4k at 40, 32.5k at
+    // 48-64, 29.9k at 128; config 4 32.2k -> 32.75k at 56.  So 56 where a
+    // chunk-plane holds >= 4 waves of tiles (configs 4, 5), else 32.
+    const bool wide = !RING && ntiles >= 4 * slots;
+    const int kMaxChunk = wide ? k2_max_chunk<T>(true) : k2_max_chunk<T>(false);
     int best = 1;
     double best_cost = 1e300;
     for (int nch = 1; nch <= nxs; ++nch) {
@@ -709,7 +718,7 @@ bool k2_supported(const SlabGeom& g) {
 // what chunk j reads); chunks <= j-2 have finished (the ticket wait).
 template <typename T>
 int k2_sc_gap() {
-    return 2 * k2_max_chunk<T>() + 4;
+    return 2 * k2_max_chunk<T>(false) + 4;
 }
 
 template <typename T>
