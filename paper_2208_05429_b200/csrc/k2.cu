@@ -4,7 +4,7 @@
 // the second collide").
 //
 // Each CTA owns an output tile T of TY x TZ cells in the (y, z) plane and
-// marches along x over a chunk of <= 32 planes (the paper's X-outermost
+// marches along x over a chunk of <= 32-56 planes (the paper's X-outermost
 // order; short chunks keep co-resident CTAs within a few planes
 // of each other, so the halo rows one CTA stages are still in L2 for its
 // neighbours).  Per input plane p:
