@@ -89,6 +89,17 @@ __host__ __device__ constexpr int wall_idx(int k, int dim, int sgn) {
     return m;
 }
 
+// periodic z-wrap lanes: position of slot k among the slots whose source
+// wraps for a lane on side 0 (c_z == s or 0) or side 1 (c_z == s), s = +-1
+__host__ __device__ constexpr int zwrap_idx(int k, int side, int s) {
+    int m = 0;
+    for (int j = 0; j < k; ++j) {
+        const int cz = can_cz(slot_dir(j));
+        if (cz == s || (side == 0 && cz == 0)) ++m;
+    }
+    return m;
+}
+
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
                  "l"(src)
@@ -307,6 +318,40 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     if (p_first <= p_last) wall_prefetch(p_first, 0);
+    // Periodic z-wrap lanes (fp64 8x32: they fit the wall buffer): in the
+    // first and the last z tile the two edge columns pull 14 / 5 values from
+    // across the z wrap, which the TMA box zero-fills.  They are prefetched
+    // one plane ahead with cp.async like the cavity wall values:
+    // [side 0: HY lanes x 14][side 1: HY lanes x 5] per buffer.
+    constexpr bool kZPre = BC == BC_PERIODIC && !RING && C::HY * kQ <= C::WALLE;  // (ring: spills)
+    const bool zlo = z0 == 0, zhi = z0 + TZ >= g.nz;
+    const bool zpre = kZPre && zlo != zhi && g.nz % TZ == 0;
+    const int zs = zlo ? 1 : -1;  // c_z of the slots that wrap on side 1
+    const int zside = !zpre || !act1 ? -1
+                      : zlo ? (b == 0 ? 0 : (b == 1 ? 1 : -1)) : (b == TZ + 1 ? 0 : (b == TZ ? 1 : -1));
+    auto zwrap_prefetch = [&](int pn, int buf) {
+        if constexpr (kZPre) {
+            if (zside < 0) return;
+            T* const wb = wallbuf + buf * C::WALLE + (zside == 0 ? a * 14 : C::HY * 14 + a * 5);
+            const int sy0 = wrapi(qy, g.ny);
+            static_for<0, kQ>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                constexpr int i = slot_dir(k);
+                constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
+                if (cz == zs || (zside == 0 && cz == 0)) {
+                    const int sy = cy == 0 ? sy0 : wrapi(qy - cy, g.ny);
+                    const T* src = A + plane_base_t<RING>(g, pn - cx) + (long long)k * g.pq +
+                                   (long long)sy * g.nzp + wrapi(qz - cz, g.nz);
+                    T* d = wb + (zs > 0 ? zwrap_idx(k, 0, 1) : zwrap_idx(k, 0, -1));
+                    if (zside == 1) d = wb + (zs > 0 ? zwrap_idx(k, 1, 1) : zwrap_idx(k, 1, -1));
+                    if constexpr (sizeof(T) == 8) cp_async8(d, src);
+                    else cp_async4(d, src);
+                }
+            });
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    };
+    if (p_first <= p_last) zwrap_prefetch(p_first, 0);
 
     // Software pipeline, ONE block barrier per plane (after the stage read).
     // Iteration p runs, in the same phase, step 2 of destination plane p-2
@@ -343,16 +388,37 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                     fs[slot_dir(k)] = sp[k * C::BOXE - can_cz(slot_dir(k))];
                 });
                 if constexpr (BC == BC_PERIODIC) {
-                    // Sources that wrap (outside [0,ny) x [0,nz)): fetched per
-                    // thread from the wrapped cell (TMA zero-filled them); no
-                    // CTA-wide fix-up pass (measured +9% over one).
-                    if ((edge_y || edge_z) && act1) {
+                    // Sources that wrap (outside [0,ny) x [0,nz)): the z-wrap
+                    // lanes' prefetched values (zwrap_prefetch), the rest
+                    // fetched per thread from the wrapped cell (TMA zero-filled
+                    // them); no CTA-wide fix-up pass (measured +9% over one).
+                    if constexpr (kZPre) {
+                        if (zside >= 0) {
+                            asm volatile("cp.async.wait_group 0;" ::: "memory");
+                            const T* const wb =
+                                wallbuf + (c & 1) * C::WALLE + (zside == 0 ? a * 14 : C::HY * 14 + a * 5);
+                            static_for<0, kQ>([&](auto kc) {
+                                constexpr int k = decltype(kc)::value;
+                                constexpr int i = slot_dir(k);
+                                constexpr int cz = can_cz(i);
+                                if (cz == zs || (zside == 0 && cz == 0)) {
+                                    const int o = zside == 0 ? (zs > 0 ? zwrap_idx(k, 0, 1) : zwrap_idx(k, 0, -1))
+                                                             : (zs > 0 ? zwrap_idx(k, 1, 1) : zwrap_idx(k, 1, -1));
+                                    fs[i] = wb[o];
+                                }
+                            });
+                        }
+                        if (p + 1 <= p_last) zwrap_prefetch(p + 1, (c + 1) & 1);
+                    }
+                    if ((edge_y || (edge_z && !zpre)) && act1) {
                         static_for<0, kQ>([&](auto kc) {
                             constexpr int k = decltype(kc)::value;
                             constexpr int i = slot_dir(k);
                             constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
                             const int sy = qy - cy, sz = qz - cz;
-                            if (sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz)
+                            // (with zpre, the z-wrapping sources came from the prefetch)
+                            const bool zw = sz < 0 || sz >= g.nz;
+                            if ((sy < 0 || sy >= g.ny || zw) && !(zpre && zw))
                                 fs[i] = A[plane_base_t<RING>(g, p - cx) + (long long)k * g.pq +
                                           (long long)wrapi(sy, g.ny) * g.nzp + wrapi(sz, g.nz)];
                         });

@@ -187,7 +187,7 @@ def test_rest_state_and_lid_closed_form():
 
 
 K2_DIMS = [(1, 8, 32), (2, 5, 7), (3, 9, 33), (7, 8, 32), (16, 16, 64), (5, 17, 31), (33, 10, 70), (12, 24, 96),
-           (64, 11, 40)]
+           (64, 11, 40), (9, 13, 64)]
 
 
 @pytest.mark.parametrize("dims", K2_DIMS)
