@@ -372,6 +372,33 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         T* const st = stage + s * kQ * C::BOXE;
         const bool lwall = BC == BC_CAVITY && p == 0 && g.left_wall;
         const bool rwall = BC == BC_CAVITY && p == g.nxl - 1 && g.right_wall;
+        // Periodic edge tiles: sources that wrap (outside [0,ny) x [0,nz); the
+        // TMA zero-filled them) are loaded per thread from the wrapped cell
+        // (no CTA-wide fix-up pass: measured +9% over one).  fp64 issues them
+        // before the stage wait so their latency overlaps it (config 3 26.7k
+        // -> 28.0k); fp32 after the stage read (early: 41.5k -> 40.8k).  With
+        // zpre the z-wrap lanes take theirs from the prefetch instead.
+        constexpr bool kEarlyWrap = sizeof(T) == 8;
+        T fs[kQ];
+        const bool wdir = BC == BC_PERIODIC && has1 && (edge_y || (edge_z && !zpre)) && act1;
+        auto wraps = [&](int cy, int cz) {
+            const int sy = qy - cy, sz = qz - cz;
+            const bool zw = sz < 0 || sz >= g.nz;
+            return (sy < 0 || sy >= g.ny || zw) && !(zpre && zw);
+        };
+        auto load_wrapped = [&] {
+            if (wdir) {
+                static_for<0, kQ>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    constexpr int i = slot_dir(k);
+                    constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
+                    if (wraps(cy, cz))
+                        fs[i] = A[plane_base_t<RING>(g, p - cx) + (long long)k * g.pq +
+                                  (long long)wrapi(qy - cy, g.ny) * g.nzp + wrapi(qz - cz, g.nz)];
+                });
+            }
+        };
+        if constexpr (BC == BC_PERIODIC && kEarlyWrap) load_wrapped();
         if (has1) {
             mbar_wait(&bar[s], uint32_t(c >> 1) & 1u);
         }
@@ -381,19 +408,18 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         // phases to land (an effective third pipeline stage without a third
         // buffer).  The barrier also orders step 1 of plane p-1 (last
         // iteration's pushes) before step 2 of plane p-2 below.
-        T fs[kQ];
         auto read_stage = [&] {
             if (has1) {
                 const T* const sp = st + (act1 ? soff : C::ZPAD);
                 static_for<0, kQ>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
-                    fs[slot_dir(k)] = sp[k * C::BOXE - can_cz(slot_dir(k))];
+                    constexpr int i = slot_dir(k);
+                    if (BC == BC_PERIODIC && kEarlyWrap && wdir && wraps(can_cy(i), can_cz(i))) return;
+                    fs[i] = sp[k * C::BOXE - can_cz(i)];
                 });
+                if constexpr (BC == BC_PERIODIC && !kEarlyWrap) load_wrapped();
                 if constexpr (BC == BC_PERIODIC) {
-                    // Sources that wrap (outside [0,ny) x [0,nz)): the z-wrap
-                    // lanes' prefetched values (zwrap_prefetch), the rest
-                    // fetched per thread from the wrapped cell (TMA zero-filled
-                    // them); no CTA-wide fix-up pass (measured +9% over one).
+                    // z-wrap lanes: their prefetched wrapped values
                     if constexpr (kZPre) {
                         if (zside >= 0) {
                             asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -411,19 +437,6 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                             });
                         }
                         if (p + 1 <= p_last) zwrap_prefetch(p + 1, (c + 1) & 1);
-                    }
-                    if ((edge_y || (edge_z && !zpre)) && act1) {
-                        static_for<0, kQ>([&](auto kc) {
-                            constexpr int k = decltype(kc)::value;
-                            constexpr int i = slot_dir(k);
-                            constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
-                            const int sy = qy - cy, sz = qz - cz;
-                            // (with zpre, the z-wrapping sources came from the prefetch)
-                            const bool zw = sz < 0 || sz >= g.nz;
-                            if ((sy < 0 || sy >= g.ny || zw) && !(zpre && zw))
-                                fs[i] = A[plane_base_t<RING>(g, p - cx) + (long long)k * g.pq +
-                                          (long long)wrapi(sy, g.ny) * g.nzp + wrapi(sz, g.nz)];
-                        });
                     }
                 }
                 if constexpr (BC == BC_CAVITY) {
