@@ -321,7 +321,7 @@ def main():
                "d2h_bytes_per_step": int(out_rho_h.numel() * 8 + out_u_h.numel() * 8) * world}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the contract: rank 0 at N=1 only
         try:
             v, threads, sample, _ = oracle_sample(cfg, 12.0)
             model, ncpu = cpu_info()
