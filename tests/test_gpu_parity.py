@@ -498,3 +498,22 @@ def test_randomised_configurations_bitwise():
         assert np.array_equal(got, want), case
         if dtype == "f64":
             assert relerr_floor(want, oracle.run(f0, bc, tau, lid, sum(splits))) <= 1e-12, case
+
+
+@pytest.mark.parametrize("kernel", [lbm.LBM_KERNEL_AUTO, lbm.LBM_KERNEL_K2_SC, lbm.LBM_KERNEL_AA])
+def test_init_null_velocity_equals_zero_velocity(kernel):
+    """u = NULL is u = 0 (include/lbm.h; bench.py passes NULL for the cavity
+    recipes' zero initial velocity): host and device inputs, every storage."""
+    cfg = li.CONFIGS[2]
+    rho, u = li.init_fields(cfg)
+    assert not np.any(u)
+    outs = []
+    with lbm.Lattice(cfg.nx, cfg.ny, cfg.nz, cfg.tau, cfg.u_lid, "f64", kernel=kernel) as lat:
+        for args in ((rho, u), (rho, None)):
+            lat.init_equilibrium(*args)
+            lat.step(5)
+            outs.append(lat.populations())
+        lbm.lbm_init_equilibrium_device(lat.ctx, torch.from_numpy(rho).cuda(), None)
+        lat.step(5)
+        outs.append(lat.populations())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
