@@ -109,8 +109,11 @@ typedef enum {
      * G planes below the slot of f*(t-1) of plane x, chunks of <= 32 (48)
      * planes taken in x order, so no plane is overwritten before its last
      * reader has finished; an odd step runs the in-place K1 the same way.
-     * Bitwise identical to K2/K1.  EINVAL at create unless world == 1 and
-     * local_slabs == 1, or where the TMA descriptor cannot describe the slab. */
+     * Bitwise identical to K2/K1.  X-slabs (LOCAL, NCCL): each slab its own
+     * ring, halo parts exchanged through the ring mapping; init and
+     * set_populations write the canonical state and invert the stream in
+     * place.  EINVAL at create where the TMA descriptor cannot describe the
+     * slab. */
     LBM_KERNEL_K2_SC = 5
 } lbm_kernel;
 

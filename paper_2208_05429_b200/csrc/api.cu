@@ -12,6 +12,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -201,24 +202,63 @@ StepParams<T> make_params(const lbm_ctx* c, const Slab& s) {
 }
 
 // ---------------------------------------------------------------- halo --
-// Single-copy ring (one slab, periodic): the x wrap onto itself, plane by
-// plane through the ring mapping -- right ghost [x=nxl: all | x=nxl+1: M]
-// <- [x=0 | x=1], left ghost [x=-2: P | x=-1: all] <- [x=nxl-2 | x=nxl-1].
+// Single-copy ring storage: the halo spans through the ring mapping, plane
+// part by plane part (a span may straddle the end of the ring) -- right
+// ghost [x=nxl: all | x=nxl+1: M] <- the right neighbour's [x=0 | x=1], left
+// ghost [x=-2: P | x=-1: all] <- the left neighbour's [x=nxl-2 | x=nxl-1];
+// the neighbour is the slab itself for a periodic single slab.  LOCAL: D2D
+// copies; NCCL: the same parts as grouped send/recv, posted in the order of
+// exchange() so the pairs match on a ring of two.
 lbm_status exchange_sc(lbm_ctx* c, cudaStream_t st) {
-    Slab& s = c->slabs[0];
-    const SlabGeom& g = s.g;
-    char* b = static_cast<char*>(s.buf[0]);
     const size_t es = c->esize;
-    auto copy = [&](int xd, int xs, int slot0, int nslots) -> cudaError_t {
-        const long long o = (long long)slot0 * g.pq;
-        return cudaMemcpyAsync(b + (plane_base(g, xd) + o) * es, b + (plane_base(g, xs) + o) * es,
-                               size_t(nslots) * g.pq * es, cudaMemcpyDeviceToDevice, st);
+    struct Part {
+        int x, slot0, nslots;
     };
-    const int n = g.nxl;
-    CK(copy(n, 0, 0, kQ));
-    CK(copy(n + 1, 1, 0, kSlotsM));
-    CK(copy(-2, n - 2, kSlotP0, kQ - kSlotP0));
-    CK(copy(-1, n - 1, 0, kQ));
+    // parts a slab sends left / receives from the right, sends right / receives from the left
+    auto parts_to_left = [](int) { return std::array<Part, 2>{{{0, 0, kQ}, {1, 0, kSlotsM}}}; };
+    auto parts_from_right = [](int n) { return std::array<Part, 2>{{{n, 0, kQ}, {n + 1, 0, kSlotsM}}}; };
+    auto parts_to_right = [](int n) { return std::array<Part, 2>{{{n - 2, kSlotP0, kQ - kSlotP0}, {n - 1, 0, kQ}}}; };
+    auto parts_from_left = [](int) { return std::array<Part, 2>{{{-2, kSlotP0, kQ - kSlotP0}, {-1, 0, kQ}}}; };
+    auto addr = [&](const Slab& s, const Part& q) {
+        return static_cast<char*>(s.buf[0]) + (plane_base(s.g, q.x) + (long long)q.slot0 * s.g.pq) * (long long)es;
+    };
+    if (c->opts.comm == LBM_COMM_NCCL) {
+        Slab& s = c->slabs[0];
+        const ncclDataType_t ty = c->dt == LBM_F64 ? ncclFloat64 : ncclFloat32;
+        const int n = s.g.nxl;
+        CKN(g_nccl.GroupStart());
+        if (s.left >= 0)
+            for (const Part& q : parts_to_left(n))
+                CKN(g_nccl.Send(addr(s, q), size_t(q.nslots) * s.g.pq, ty, s.left, c->comm, st));
+        if (s.right >= 0)
+            for (const Part& q : parts_from_right(n))
+                CKN(g_nccl.Recv(addr(s, q), size_t(q.nslots) * s.g.pq, ty, s.right, c->comm, st));
+        if (s.right >= 0)
+            for (const Part& q : parts_to_right(n))
+                CKN(g_nccl.Send(addr(s, q), size_t(q.nslots) * s.g.pq, ty, s.right, c->comm, st));
+        if (s.left >= 0)
+            for (const Part& q : parts_from_left(n))
+                CKN(g_nccl.Recv(addr(s, q), size_t(q.nslots) * s.g.pq, ty, s.left, c->comm, st));
+        CKN(g_nccl.GroupEnd());
+        return LBM_OK;
+    }
+    for (Slab& s : c->slabs) {
+        const int n = s.g.nxl;
+        if (s.right >= 0) {
+            const Slab& R = c->slabs[s.right];
+            const auto src = parts_to_left(R.g.nxl), dst = parts_from_right(n);
+            for (int k = 0; k < 2; ++k)
+                CK(cudaMemcpyAsync(addr(s, dst[k]), addr(R, src[k]), size_t(dst[k].nslots) * s.g.pq * es,
+                                   cudaMemcpyDeviceToDevice, st));
+        }
+        if (s.left >= 0) {
+            const Slab& L = c->slabs[s.left];
+            const auto src = parts_to_right(L.g.nxl), dst = parts_from_left(n);
+            for (int k = 0; k < 2; ++k)
+                CK(cudaMemcpyAsync(addr(s, dst[k]), addr(L, src[k]), size_t(dst[k].nslots) * s.g.pq * es,
+                                   cudaMemcpyDeviceToDevice, st));
+        }
+    }
     return LBM_OK;
 }
 
@@ -434,8 +474,6 @@ lbm_status run_steps_aa(lbm_ctx* c, long n) {
 // by the in-place K1; each shifts the state window down the ring
 template <typename T>
 lbm_status run_steps_sc(lbm_ctx* c, long n) {
-    Slab& s = c->slabs[0];
-    T* F = static_cast<T*>(s.buf[0]);
     while (n > 0) {
         const int nsteps = n >= 2 ? 2 : 1;
         lbm_status st = ensure_ghosts(c);
@@ -443,21 +481,51 @@ lbm_status run_steps_sc(lbm_ctx* c, long n) {
         size_t slot = 0;
         st = prof_begin(c, slot);
         if (st != LBM_OK) return st;
-        const StepParams<T> P = make_params<T>(c, s);
-        const int shift = nsteps == 2 ? c->sc_gap : kK1ScGap;
-        const int out_poff = (s.g.poff - shift + s.g.pmod) % s.g.pmod;
-        cudaError_t e = nsteps == 2 ? launch_k2<T>(F, F, P, 0, s.g.nxl, c->stream, out_poff, c->sc_sync)
-                                    : launch_k1_sc<T>(F, P, out_poff, c->sc_sync, c->stream);
-        if (e != cudaSuccess) return fail(c, LBM_ECUDA, "single-copy sweep launch failed: %s", cudaGetErrorString(e));
-        c->launches++;
-        (nsteps == 2 ? c->k2_launches : c->k1_launches)++;
-        st = prof_end(c, slot, (long long)nsteps * s.g.nxl * s.g.ny * s.g.nz);
+        long long updates = 0;
+        // slabs one after another on the stream (the ticket words are reused)
+        for (Slab& s : c->slabs) {
+            T* F = static_cast<T*>(s.buf[0]);
+            const StepParams<T> P = make_params<T>(c, s);
+            const int shift = nsteps == 2 ? c->sc_gap : kK1ScGap;
+            const int out_poff = (s.g.poff - shift + s.g.pmod) % s.g.pmod;
+            cudaError_t e = nsteps == 2 ? launch_k2<T>(F, F, P, 0, s.g.nxl, c->stream, out_poff, c->sc_sync)
+                                        : launch_k1_sc<T>(F, P, out_poff, c->sc_sync, c->stream);
+            if (e != cudaSuccess)
+                return fail(c, LBM_ECUDA, "single-copy sweep launch failed: %s", cudaGetErrorString(e));
+            c->launches++;
+            (nsteps == 2 ? c->k2_launches : c->k1_launches)++;
+            updates += (long long)nsteps * s.g.nxl * s.g.ny * s.g.nz;
+            s.g.poff = out_poff;
+        }
+        st = prof_end(c, slot, updates);
         if (st != LBM_OK) return st;
-        s.g.poff = out_poff;
         c->ghosts_valid = false;
         c->t += nsteps;
         n -= nsteps;
     }
+    return LBM_OK;
+}
+
+// X-slab single-copy contexts: the canonical f(t0) has been written into
+// every slab's ring window -> exchange its ghosts -> the inverse stream in
+// place (launch_k1_sc with unstream, shifting the window like a K1 step).
+template <typename T>
+lbm_status sc_finish_canonical(lbm_ctx* c) {
+    c->ghosts_valid = false;
+    lbm_status st = ensure_ghosts(c);
+    if (st != LBM_OK) return st;
+    for (Slab& s : c->slabs) {
+        const StepParams<T> P = make_params<T>(c, s);
+        const int out_poff = (s.g.poff - kK1ScGap + s.g.pmod) % s.g.pmod;
+        cudaError_t e = launch_k1_sc<T>(static_cast<T*>(s.buf[0]), P, out_poff, c->sc_sync, c->stream, true);
+        if (e != cudaSuccess) return fail(c, LBM_ECUDA, "single-copy unstream failed: %s", cudaGetErrorString(e));
+        c->launches++;
+        s.g.poff = out_poff;
+    }
+    c->cur = 0;
+    c->ghosts_valid = false;
+    c->initialized = true;
+    c->t = 0;
     return LBM_OK;
 }
 
@@ -678,6 +746,47 @@ lbm_status sc_init_done(lbm_ctx* c) {
 
 template <typename T>
 lbm_status init_eq_sc(lbm_ctx* c, const double* rho, const double* u, bool host) {
+    if (c->slabs.size() > 1 || c->opts.world > 1) {
+        // X-slabs: canonical feq into each window (K0a, chunked through the
+        // staging buffer for host inputs), then exchange + in-place unstream
+        const long long plane = (long long)c->ny * c->nz;
+        const int cap = int(std::max<long long>(1, (long long)(c->stage_bytes / (4 * sizeof(double))) / plane));
+        double* stage = static_cast<double*>(c->stage);
+        c->initialized = false;
+        for (Slab& s : c->slabs) {
+            T* F = static_cast<T*>(s.buf[0]);
+            const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;
+            if (!host) {
+                CK(launch_k0_equilibrium<T>(rho ? rho + xoff : nullptr, u ? u + 3 * xoff : nullptr, F, s.g, c->stream));
+                c->launches++;
+                continue;
+            }
+            for (int xb = 0; xb < s.g.nxl; xb += cap) {
+                const int nxc = std::min(cap, s.g.nxl - xb);
+                const long long cells = (long long)nxc * plane, hoff = xoff + (long long)xb * plane;
+                const double* dr = nullptr;
+                const double* du = nullptr;
+                if (rho) {
+                    CK(cudaMemcpyAsync(stage, rho + hoff, cells * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+                    dr = stage;
+                }
+                if (u) {
+                    CK(cudaMemcpyAsync(stage + cells, u + 3 * hoff, 3 * cells * sizeof(double),
+                                       cudaMemcpyHostToDevice, c->stream));
+                    du = stage + cells;
+                }
+                int flag = 0;
+                lbm_status st;
+                if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
+                if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+                if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
+                if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+                CK(launch_k0_equilibrium<T>(dr, du, F, s.g, c->stream, xb, nxc));
+                c->launches++;
+            }
+        }
+        return sc_finish_canonical<T>(c);
+    }
     Slab& s = c->slabs[0];
     const StepParams<T> P = make_params<T>(c, s);
     T* F = static_cast<T*>(s.buf[0]);
@@ -718,6 +827,31 @@ lbm_status init_eq_sc(lbm_ctx* c, const double* rho, const double* u, bool host)
 
 template <typename T>
 lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
+    if (c->slabs.size() > 1 || c->opts.world > 1) {
+        // X-slabs: canonical f into each window (K0 import, chunked), then
+        // exchange + in-place unstream
+        const long long plane = (long long)c->ny * c->nz;
+        const long long proc_cells = (long long)c->nxl_proc * plane;
+        const int cap = int(std::max<long long>(1, (long long)(c->stage_bytes / (kQ * sizeof(double))) / plane));
+        double* stage = static_cast<double*>(c->stage);
+        c->initialized = false;
+        for (Slab& s : c->slabs) {
+            for (int xb = 0; xb < s.g.nxl; xb += cap) {
+                const int nxc = std::min(cap, s.g.nxl - xb);
+                const long long ccells = (long long)nxc * plane;
+                const double* src = f + (long long)(s.g.x0 - c->x0_proc + xb) * plane;
+                CK(cudaMemcpy2DAsync(stage, ccells * sizeof(double), src, proc_cells * sizeof(double),
+                                     ccells * sizeof(double), kQ, cudaMemcpyHostToDevice, c->stream));
+                int flag = 0;
+                lbm_status st = validate_device(c, stage, kQ * ccells, false, &flag);
+                if (st != LBM_OK) return st;
+                if (flag) return fail(c, LBM_EINVAL, "populations must be finite (state is now undefined)");
+                CK(launch_k0_import<T>(stage, static_cast<T*>(s.buf[0]), s.g, xb, nxc, c->stream));
+                c->launches++;
+            }
+        }
+        return sc_finish_canonical<T>(c);
+    }
     Slab& s = c->slabs[0];
     const StepParams<T> P = make_params<T>(c, s);
     T* F = static_cast<T*>(s.buf[0]);
@@ -1015,8 +1149,6 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     if (o.comm == LBM_COMM_LOCAL && o.world != 1) return fail(c, LBM_EINVAL, "comm LOCAL needs world == 1");
     if (o.comm < LBM_COMM_NONE || o.comm > LBM_COMM_LOCAL) return fail(c, LBM_EINVAL, "bad comm %d", o.comm);
     if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K2_SC) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
-    if (o.kernel == LBM_KERNEL_K2_SC && (o.world != 1 || o.local_slabs != 1))
-        return fail(c, LBM_EINVAL, "kernel K2_SC needs a single slab (world == 1, local_slabs == 1)");
     if (o.kernel == LBM_KERNEL_AA && o.bc == LBM_BC_CAVITY && (o.world > 1 || o.local_slabs > 1) &&
         nx / (o.world * o.local_slabs) < 2)
         return fail(c, LBM_EINVAL, "kernel AA with X-slabs needs >= 2 planes per slab");

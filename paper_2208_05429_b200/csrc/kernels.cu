@@ -37,7 +37,12 @@ __global__ void __launch_bounds__(256) k1_step(const T* __restrict__ A, T* __res
 // x - 4 (out_poff = poff - 4).  Tiles are taken by ticket in plane order; a
 // tile of plane x waits until planes x-3, x-4, x-5 are finished (so, by
 // induction, every plane <= x-3, the last readers of plane x-4).
-template <typename T, int BC>
+template <typename T, int BC, int k>
+__device__ __forceinline__ T unstream_slot(const T* C, const StepParams<T>& P, int x, int y, int z, long long self);
+
+// UNSTREAM: instead of a step, K0b's inverse stream of a canonical state held
+// in the ring (X-slab single-copy init / set_populations), same ring shift.
+template <typename T, int BC, bool UNSTREAM = false>
 __global__ void __launch_bounds__(256) k1_step_sc(T* F, StepParams<T> P, int out_poff, unsigned* sync, int tiles_z,
                                                  int tpp) {
     __shared__ int s_item;
@@ -53,15 +58,28 @@ __global__ void __launch_bounds__(256) k1_step_sc(T* F, StepParams<T> P, int out
     const int z = (tile % tiles_z) * 32 + threadIdx.x;
     const int y = (tile / tiles_z) * 8 + threadIdx.y;
     if (z < P.g.nz && y < P.g.ny) {
-        T f[kQ];
-        pull_cell<T, BC>(F, P, x, y, z, f);
-        bgk_collide<T>(f, P.omega);
         const int ps = x + 2 + out_poff;
         T* const dst = F + (long long)(ps >= P.g.pmod ? ps - P.g.pmod : ps) * P.g.px + (long long)y * P.g.nzp + z;
-        static_for<0, kQ>([&](auto kc) {
-            constexpr int k = decltype(kc)::value;
-            __stcs(dst + (long long)k * P.g.pq, f[slot_dir(k)]);
-        });
+        if constexpr (UNSTREAM) {
+            T v[kQ];
+            const long long self = cell_off(P.g, x, y, z);
+            static_for<0, kQ>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                v[k] = unstream_slot<T, BC, k>(F, P, x, y, z, self);
+            });
+            static_for<0, kQ>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                __stcs(dst + (long long)k * P.g.pq, v[k]);
+            });
+        } else {
+            T f[kQ];
+            pull_cell<T, BC>(F, P, x, y, z, f);
+            bgk_collide<T>(f, P.omega);
+            static_for<0, kQ>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                __stcs(dst + (long long)k * P.g.pq, f[slot_dir(k)]);
+            });
+        }
     }
     __syncthreads();  // every thread's stores, then one cumulative fence and the count
     if (threadIdx.x == 0 && threadIdx.y == 0) {
@@ -102,6 +120,39 @@ __global__ void __launch_bounds__(256) k0_equilibrium(const double* __restrict__
 //   f_j(y + c_j)                              if y + c_j is a cell (or ghost / wrap)
 //   f_opp(j)(y) - [(y + c_j)_z >= nz] lid_opp(j)  if y + c_j is beyond a wall.
 // C must have valid ghost planes.
+template <typename T, int BC, int k>
+__device__ __forceinline__ T unstream_slot(const T* C, const StepParams<T>& P, int x, int y, int z, long long self) {
+    const SlabGeom& g = P.g;
+    constexpr int j = slot_dir(k);
+    constexpr int cx = can_cx(j), cy = can_cy(j), cz = can_cz(j);
+    int ty = y + cy, tz = z + cz;
+    bool wall = false;
+    if constexpr (BC == BC_CAVITY) {
+        if constexpr (cx == -1) wall = wall || (x == 0 && g.left_wall);
+        if constexpr (cx == 1) wall = wall || (x == g.nxl - 1 && g.right_wall);
+        if constexpr (cy == -1) wall = wall || (y == 0);
+        if constexpr (cy == 1) wall = wall || (y == g.ny - 1);
+        if constexpr (cz == -1) wall = wall || (z == 0);
+        if constexpr (cz == 1) wall = wall || (z == g.nz - 1);
+    } else {
+        if constexpr (cy == -1) ty = (y == 0) ? g.ny - 1 : ty;
+        if constexpr (cy == 1) ty = (y == g.ny - 1) ? 0 : ty;
+        if constexpr (cz == -1) tz = (z == 0) ? g.nz - 1 : tz;
+        if constexpr (cz == 1) tz = (z == g.nz - 1) ? 0 : tz;
+    }
+    T v;
+    if (!wall) {
+        v = C[plane_base(g, x + cx) + (long long)k * g.pq + (long long)ty * g.nzp + tz];
+    } else {
+        constexpr int ko = slot_opp(k);
+        v = C[self + (long long)ko * g.pq];
+        if constexpr (cz == 1) {
+            if (z == g.nz - 1) v = v - P.lid[ko];
+        }
+    }
+    return v;
+}
+
 template <typename T, int BC>
 __global__ void __launch_bounds__(256) k0_unstream(const T* __restrict__ C, T* __restrict__ A, StepParams<T> P) {
     const int z = blockIdx.x * 32 + threadIdx.x;
@@ -112,34 +163,7 @@ __global__ void __launch_bounds__(256) k0_unstream(const T* __restrict__ C, T* _
     const long long self = cell_off(g, x, y, z);
     static_for<0, kQ>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
-        constexpr int j = slot_dir(k);
-        constexpr int cx = can_cx(j), cy = can_cy(j), cz = can_cz(j);
-        int ty = y + cy, tz = z + cz;
-        bool wall = false;
-        if constexpr (BC == BC_CAVITY) {
-            if constexpr (cx == -1) wall = wall || (x == 0 && g.left_wall);
-            if constexpr (cx == 1) wall = wall || (x == g.nxl - 1 && g.right_wall);
-            if constexpr (cy == -1) wall = wall || (y == 0);
-            if constexpr (cy == 1) wall = wall || (y == g.ny - 1);
-            if constexpr (cz == -1) wall = wall || (z == 0);
-            if constexpr (cz == 1) wall = wall || (z == g.nz - 1);
-        } else {
-            if constexpr (cy == -1) ty = (y == 0) ? g.ny - 1 : ty;
-            if constexpr (cy == 1) ty = (y == g.ny - 1) ? 0 : ty;
-            if constexpr (cz == -1) tz = (z == 0) ? g.nz - 1 : tz;
-            if constexpr (cz == 1) tz = (z == g.nz - 1) ? 0 : tz;
-        }
-        T v;
-        if (!wall) {
-            v = C[plane_base(g, x + cx) + (long long)k * g.pq + (long long)ty * g.nzp + tz];
-        } else {
-            constexpr int ko = slot_opp(k);
-            v = C[self + (long long)ko * g.pq];
-            if constexpr (cz == 1) {
-                if (z == g.nz - 1) v = v - P.lid[ko];
-            }
-        }
-        A[self + (long long)k * g.pq] = v;
+        A[self + (long long)k * g.pq] = unstream_slot<T, BC, k>(C, P, x, y, z, self);
     });
 }
 
@@ -339,17 +363,24 @@ cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
 }
 
 template <typename T>
-cudaError_t launch_k1_sc(T* F, const StepParams<T>& P, int out_poff, unsigned* sync, cudaStream_t s) {
+cudaError_t launch_k1_sc(T* F, const StepParams<T>& P, int out_poff, unsigned* sync, cudaStream_t s, bool unstream) {
     const SlabGeom& g = P.g;
     if (g.nxl <= 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(sync, 0, sizeof(unsigned) * (1 + g.nxl), s);
     if (e != cudaSuccess) return e;
     const int tiles_z = (g.nz + 31) / 32, tpp = tiles_z * ((g.ny + 7) / 8);
     const unsigned grid = unsigned((long long)tpp * g.nxl);
-    if (g.bc == BC_PERIODIC)
-        k1_step_sc<T, BC_PERIODIC><<<grid, kBlock, 0, s>>>(F, P, out_poff, sync, tiles_z, tpp);
-    else
-        k1_step_sc<T, BC_CAVITY><<<grid, kBlock, 0, s>>>(F, P, out_poff, sync, tiles_z, tpp);
+    if (unstream) {
+        if (g.bc == BC_PERIODIC)
+            k1_step_sc<T, BC_PERIODIC, true><<<grid, kBlock, 0, s>>>(F, P, out_poff, sync, tiles_z, tpp);
+        else
+            k1_step_sc<T, BC_CAVITY, true><<<grid, kBlock, 0, s>>>(F, P, out_poff, sync, tiles_z, tpp);
+    } else {
+        if (g.bc == BC_PERIODIC)
+            k1_step_sc<T, BC_PERIODIC><<<grid, kBlock, 0, s>>>(F, P, out_poff, sync, tiles_z, tpp);
+        else
+            k1_step_sc<T, BC_CAVITY><<<grid, kBlock, 0, s>>>(F, P, out_poff, sync, tiles_z, tpp);
+    }
     return cudaGetLastError();
 }
 
@@ -418,7 +449,7 @@ cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int 
 
 #define LBM_INSTANTIATE(T)                                                                                   \
     template cudaError_t launch_k1<T>(const T*, T*, const StepParams<T>&, int, int, cudaStream_t);           \
-    template cudaError_t launch_k1_sc<T>(T*, const StepParams<T>&, int, unsigned*, cudaStream_t);            \
+    template cudaError_t launch_k1_sc<T>(T*, const StepParams<T>&, int, unsigned*, cudaStream_t, bool);      \
     template cudaError_t launch_k0_equilibrium<T>(const double*, const double*, T*, const SlabGeom&,         \
                                                   cudaStream_t, int, int);                                   \
     template cudaError_t launch_k0_unstream<T>(const T*, T*, const StepParams<T>&, cudaStream_t);            \

@@ -13,8 +13,11 @@ cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
 // K1 in place on single-copy ring storage: output plane x to ring slot
 // x + 2 + out_poff (= the slot of input plane x - 4); sync = device scratch
 // of nxl + 1 words.
+// unstream = true: K0b's inverse stream of the canonical state in the ring
+// instead of a step (X-slab single-copy init / set_populations).
 template <typename T>
-cudaError_t launch_k1_sc(T* F, const StepParams<T>& P, int out_poff, unsigned* sync, cudaStream_t s);
+cudaError_t launch_k1_sc(T* F, const StepParams<T>& P, int out_poff, unsigned* sync, cudaStream_t s,
+                         bool unstream = false);
 constexpr int kK1ScGap = 4;
 
 // K2: two fused steps, A = f*(t-1) -> B = f*(t+1) on planes [xbeg, xbeg+nxs).

@@ -74,8 +74,8 @@ def test_create_rejects_bad_kernel_choices():
     o.kernel = 6
     with pytest.raises(lbm.LbmError, match="bad kernel"):
         lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
-    o.kernel, o.comm, o.local_slabs = lbm.LBM_KERNEL_K2_SC, lbm.LBM_COMM_LOCAL, 2
-    with pytest.raises(lbm.LbmError, match="K2_SC needs a single slab"):
+    o.kernel = -1
+    with pytest.raises(lbm.LbmError, match="bad kernel"):
         lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
 
 

@@ -401,13 +401,16 @@ def test_nccl_transport_world1_periodic_bitwise(dtype):
     except lbm.LbmError as e:  # pragma: no cover
         pytest.skip(f"NCCL unavailable: {e}")
     outs = []
-    for comm, kw in [(lbm.LBM_COMM_NONE, {}), (lbm.LBM_COMM_NCCL, {"nccl_id": uid})]:
-        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=lbm.LBM_BC_PERIODIC, comm=comm, **kw) as lat:
+    # (and the single-copy ring's halo parts through NCCL: K2_SC)
+    # (a unique id initialises one communicator: a fresh one per NCCL context)
+    for comm, kernel, kw in [(lbm.LBM_COMM_NONE, 0, {}), (lbm.LBM_COMM_NCCL, 0, {"nccl_id": uid}),
+                             (lbm.LBM_COMM_NCCL, lbm.LBM_KERNEL_K2_SC, {"nccl_id": lbm.lbm_nccl_unique_id()})]:
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=lbm.LBM_BC_PERIODIC, comm=comm, kernel=kernel, **kw) as lat:
             lat.set_populations(f0)
             lat.step(3)
             lat.step(2)
             outs.append(lat.populations())
-    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
     assert relerr_floor(outs[1], oracle.run(f0, lbm.LBM_BC_PERIODIC, 0.6, LID, 5)) <= TOL[dtype]
 
 

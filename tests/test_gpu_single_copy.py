@@ -110,9 +110,9 @@ def test_single_copy_chunked_host_transfers(bc, dtype, monkeypatch):
         assert relerr_floor(outs[SC][4], want_c) <= (1e-15 if dtype == "f64" else 1e-7)
 
 
-def test_single_copy_memory_and_errors():
+def test_single_copy_memory():
     """The ring holds one lattice copy plus G planes and a staging buffer:
-    well under the two-buffer footprint; K2_SC refuses X-slab contexts."""
+    well under the two-buffer footprint."""
     dims = (512, 128, 128)
     used = {}
     for kernel in (lbm.LBM_KERNEL_AUTO, SC):
@@ -127,8 +127,45 @@ def test_single_copy_memory_and_errors():
     lattice = (dims[0] + 4) * 19 * dims[1] * dims[2] * 8
     assert used[lbm.LBM_KERNEL_AUTO] >= 2 * lattice
     assert used[SC] <= 1.25 * lattice, used
-    with pytest.raises(lbm.LbmError):
-        lbm.Lattice(16, 8, 8, 0.6, LID, "f64", kernel=SC, comm=lbm.LBM_COMM_LOCAL, local_slabs=2)
+
+
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
+@pytest.mark.parametrize("slabs", [2, 4])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_single_copy_x_slabs_bitwise(bc, slabs, dtype, monkeypatch):
+    """K2_SC over X-slabs (LOCAL transport: each slab its own ring, halo
+    parts copied through the ring mapping; init and set_populations as the
+    canonical state plus an in-place inverse stream) equals the single-slab
+    two-buffer run bit for bit after every split, for host and device
+    initialisation and a chunked staging buffer."""
+    dims = (48, 12, 40)
+    lid = LID if bc == lbm.LBM_BC_CAVITY else (0.0, 0.0, 0.0)
+    f0 = li.random_populations(77, *dims)
+    n = dims[0] * dims[1] * dims[2]
+    rho = (1.0 + li.uniform(83, n, -1e-3, 1e-3)).reshape(dims)
+    u = li.uniform(84, 3 * n, -0.01, 0.01).reshape(*dims, 3)
+    runs = []
+    for kernel, kw in ((lbm.LBM_KERNEL_AUTO, {}), (SC, dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=slabs))):
+        if kernel == SC:
+            monkeypatch.setenv("LBM_STAGE_BYTES", "1")
+        with lbm.Lattice(*dims, 0.6, lid, dtype, bc=bc, kernel=kernel, **kw) as lat:
+            out = []
+            lat.set_populations(f0)
+            out.append(lat.populations())
+            for k in (3, 2, 5):
+                lat.step(k)
+                out.append(lat.populations())
+                out.extend(lat.macroscopic())
+            lat.init_equilibrium(rho, u)
+            lat.step(4)
+            out.append(lat.populations())
+            lbm.lbm_init_equilibrium_device(lat.ctx, torch.from_numpy(rho).cuda(), torch.from_numpy(u).cuda())
+            lat.step(1)
+            out.append(lat.populations())
+            runs.append(out)
+        monkeypatch.delenv("LBM_STAGE_BYTES", raising=False)
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)
 
 
 def test_single_copy_randomised_bitwise():
