@@ -138,7 +138,8 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    per = max(1.0, 40.0 / max(1, args.steps + args.warmup))  # whole run ~ a minute
+    budget = float(os.environ.get("LBM_REF_BUDGET_S", "40"))  # (tests shorten it)
+    per = max(min(1.0, budget), budget / max(1, args.steps + args.warmup))  # whole run ~ a minute
     for _ in range(args.warmup):
         oracle_sample(cfg, per)
     vals, secs = [], 0.0
