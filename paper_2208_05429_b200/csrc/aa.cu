@@ -34,9 +34,11 @@ namespace {
 // (x, y, z) along a compile-time direction, or -1 if that neighbour lies
 // beyond a cavity wall.  Only the axes the direction moves along are
 // tested (periodic: wrapped), like pull_src() for K1.
+// `self` = cell_off(g, x, y, z); the result is self plus a displacement
+// (AA storage never uses the single-copy plane ring, so planes are linear).
 template <int BC, int dx, int dy, int dz>
-__device__ __forceinline__ long long aa_nbr(const SlabGeom& g, int x, int y, int z, int slot) {
-    int nx_ = x + dx, ny_ = y + dy, nz_ = z + dz;
+__device__ __forceinline__ long long aa_nbr(const SlabGeom& g, int x, int y, int z, int slot, long long self) {
+    long long d = (long long)slot * g.pq;
     if constexpr (BC == BC_CAVITY) {
         bool out = false;
         // x: a wall only at the slab ends that are domain walls; otherwise
@@ -48,16 +50,19 @@ __device__ __forceinline__ long long aa_nbr(const SlabGeom& g, int x, int y, int
         if constexpr (dz == -1) out = out || z == 0;
         if constexpr (dz == 1) out = out || z == g.nz - 1;
         if (out) return -1;
+        if constexpr (dx != 0) d += dx > 0 ? g.px : -g.px;
+        if constexpr (dy != 0) d += dy > 0 ? g.nzp : -g.nzp;
+        if constexpr (dz != 0) d += dz;
     } else {
         // x wraps in the kernel only for a single slab; slabs use ghost planes
-        if constexpr (dx == -1) nx_ = (x == 0 && g.nxl == g.nx) ? g.nxl - 1 : nx_;
-        if constexpr (dx == 1) nx_ = (x == g.nxl - 1 && g.nxl == g.nx) ? 0 : nx_;
-        if constexpr (dy == -1) ny_ = y == 0 ? g.ny - 1 : ny_;
-        if constexpr (dy == 1) ny_ = y == g.ny - 1 ? 0 : ny_;
-        if constexpr (dz == -1) nz_ = z == 0 ? g.nz - 1 : nz_;
-        if constexpr (dz == 1) nz_ = z == g.nz - 1 ? 0 : nz_;
+        if constexpr (dx == -1) d += (x == 0 && g.nxl == g.nx) ? (long long)(g.nxl - 1) * g.px : -g.px;
+        if constexpr (dx == 1) d += (x == g.nxl - 1 && g.nxl == g.nx) ? -(long long)(g.nxl - 1) * g.px : g.px;
+        if constexpr (dy == -1) d += y == 0 ? (long long)(g.ny - 1) * g.nzp : -(long long)g.nzp;
+        if constexpr (dy == 1) d += y == g.ny - 1 ? -(long long)(g.ny - 1) * g.nzp : (long long)g.nzp;
+        if constexpr (dz == -1) d += z == 0 ? g.nz - 1 : -1;
+        if constexpr (dz == 1) d += z == g.nz - 1 ? -(g.nz - 1) : 1;
     }
-    return cell_off(g, nx_, ny_, nz_) + (long long)slot * g.pq;
+    return self + d;
 }
 
 // canonical f(x, t) from F: at rest (even) or after an even step (odd)
@@ -74,7 +79,7 @@ __device__ __forceinline__ void aa_gather(const T* __restrict__ F, const StepPar
         if (!odd) {
             v = F[self + (long long)k * g.pq];
         } else {
-            const long long src = aa_nbr<BC, -cx, -cy, -cz>(g, x, y, z, slot_opp(k));
+            const long long src = aa_nbr<BC, -cx, -cy, -cz>(g, x, y, z, slot_opp(k), self);
             if (src >= 0) {
                 v = F[src];
             } else {
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(256) k_aa_odd(T* __restrict__ F, StepParams<T>
         constexpr int k = decltype(kc)::value;
         constexpr int i = slot_dir(k);
         constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
-        const long long dst = aa_nbr<BC, cx, cy, cz>(g, x, y, z, k);
+        const long long dst = aa_nbr<BC, cx, cy, cz>(g, x, y, z, k, self);
         if (dst >= 0) {
             F[dst] = f[i];
         } else {
