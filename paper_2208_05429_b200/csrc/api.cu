@@ -735,7 +735,6 @@ lbm_status sc_stage_window(lbm_ctx* c, const double* host, ScWindow w, long long
     return LBM_OK;
 }
 
-template <typename T>
 lbm_status sc_init_done(lbm_ctx* c) {
     c->cur = 0;
     c->ghosts_valid = false;
@@ -793,7 +792,7 @@ lbm_status init_eq_sc(lbm_ctx* c, const double* rho, const double* u, bool host)
     if (!host) {
         CK(launch_k0_init_pull<T>(rho, u, nullptr, F, P, 0, s.g.nxl, 0, s.g.nxl, c->stream));
         c->launches++;
-        return sc_init_done<T>(c);
+        return sc_init_done(c);
     }
     const long long plane = (long long)c->ny * c->nz;
     // planes per chunk: 32 B (rho + u) per cell, two halo planes
@@ -822,7 +821,7 @@ lbm_status init_eq_sc(lbm_ctx* c, const double* rho, const double* u, bool host)
         CK(launch_k0_init_pull<T>(dr, du, nullptr, F, P, xb, nxc, w.w0, w.wn, c->stream));
         c->launches++;
     }
-    return sc_init_done<T>(c);
+    return sc_init_done(c);
 }
 
 template <typename T>
@@ -872,7 +871,7 @@ lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
         CK(launch_k0_init_pull<T>(nullptr, nullptr, stage, F, P, xb, nxc, w.w0, w.wn, c->stream));
         c->launches++;
     }
-    return sc_init_done<T>(c);
+    return sc_init_done(c);
 }
 
 template <typename T>

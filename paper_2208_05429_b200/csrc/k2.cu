@@ -802,10 +802,6 @@ int k2_sc_gap() {
     return 2 * k2_max_chunk<T>(false) + 4;
 }
 
-template <typename T>
-int k2_sc_max_chunks(int nxl) {
-    return nxl;  // chunks of >= 1 plane
-}
 
 template <typename T>
 cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s, int out_poff,
@@ -859,7 +855,5 @@ template cudaError_t launch_k2<float>(const float*, float*, const StepParams<flo
                                       unsigned*, float*, float*);
 template int k2_sc_gap<double>();
 template int k2_sc_gap<float>();
-template int k2_sc_max_chunks<double>(int);
-template int k2_sc_max_chunks<float>(int);
 
 }  // namespace lbm

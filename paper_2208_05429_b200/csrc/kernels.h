@@ -24,7 +24,7 @@ constexpr int kK1ScGap = 4;
 // A's two ghost planes per side must be valid.  Output plane d goes to ring
 // slot d + 2 + out_poff (mod P.g.pmod).  Single-copy ring storage: B == A,
 // out_poff = P.g.poff - k2_sc_gap (mod pmod), and sc_sync = device scratch of
-// k2_sc_max_chunks(nxl) + 1 words (the chunk-ordered tickets).
+// nxl + 1 words (the chunk-ordered tickets: at most one chunk per plane).
 // Fused halo (two-buffer storage only): halo_left / halo_right = the next-sweep
 // buffer of the left / right neighbour slab (or this slab's own, periodic
 // single slab), which then receives its ghost planes from this sweep's stores.
@@ -33,8 +33,6 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
                       unsigned* sc_sync = nullptr, T* halo_left = nullptr, T* halo_right = nullptr);
 template <typename T>
 int k2_sc_gap();
-template <typename T>
-int k2_sc_max_chunks(int nxl);
 template <typename T>
 bool k2_supported(const SlabGeom& g);
 // K2R: the same two-step sweep with register-staged gathers and two warp
