@@ -38,6 +38,8 @@
  *              the context is poisoned and every later call except
  *              lbm_last_error / lbm_destroy returns LBM_ESTATE.  Errors of
  *              asynchronous work surface at the next blocking call.
+ *              LBM_ENUMERIC from a blocking read-back of degenerate or
+ *              non-finite moments (the context stays usable).
  *  Threads     a context is not thread-safe; distinct contexts are
  *              independent.
  */
@@ -204,7 +206,9 @@ lbm_status lbm_nccl_unique_id(void *out128);
  * and counts are in ELEMENTS of the slab buffer (dtype-sized), which is
  * laid out as planes p = 0 .. nx_local+3 (slab-local x = p - 2, two ghost
  * planes per side), each plane [19 internal directions][ny][nz_pitch]
- * (DESIGN.md "Data layout").  A neighbour of -1 means a wall (no exchange). */
+ * (the two-buffer storage -- LBM_KERNEL_K2_SC
+ * keeps the same planes on a ring and moves the same spans in plane parts).
+ * A neighbour of -1 means a wall (no exchange). */
 typedef struct {
     int nx_local, x0;
     int nz_pitch;            /* z row pitch in elements */
