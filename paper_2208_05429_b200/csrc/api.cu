@@ -106,6 +106,9 @@ struct lbm_ctx {
     int sc_gap = 0;
     unsigned* sc_sync = nullptr;
     bool fused_halo = true;  // K2 stores the neighbours' ghost planes itself (run_steps)
+    // host read-back: moments of x chunk j+1 overlap the D2H of chunk j
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> chunk_events;
     ncclComm_t comm = nullptr;
     size_t esize = 8;
     int* d_flag = nullptr;
@@ -1021,15 +1024,29 @@ lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
         const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;
         const T* A = static_cast<const T*>(s.buf[c->cur]);
         if (host) {
+            // x chunks: the moments of chunk j+1 run while chunk j crosses PCIe
+            // on the copy stream (the staging buffer holds the whole slab)
             double* stage = static_cast<double*>(s.buf[c->cur ^ 1]);
-            CK(launch_k3_moments<T>(A, P, 0, s.g.nxl, rho ? stage : nullptr, u ? stage + cells : nullptr,
-                                    c->stream, flag));
-            c->launches++;
-            if (rho)
-                CK(cudaMemcpyAsync(rho + xoff, stage, cells * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-            if (u)
-                CK(cudaMemcpyAsync(u + 3 * xoff, stage + cells, 3 * cells * sizeof(double), cudaMemcpyDeviceToHost,
-                                   c->stream));
+            const int nch = int(std::min<size_t>(c->chunk_events.size() - 1, size_t(s.g.nxl)));
+            const int per = (s.g.nxl + nch - 1) / nch;
+            for (int j = 0, xb = 0; xb < s.g.nxl; ++j, xb += per) {
+                const int nxc = std::min(per, s.g.nxl - xb);
+                const long long o = (long long)xb * plane, cc = (long long)nxc * plane;
+                CK(launch_k3_moments<T>(A, P, xb, nxc, rho ? stage + o : nullptr, u ? stage + cells + 3 * o : nullptr,
+                                        c->stream, flag));
+                c->launches++;
+                CK(cudaEventRecord(c->chunk_events[j], c->stream));
+                CK(cudaStreamWaitEvent(c->copy_stream, c->chunk_events[j], 0));
+                if (rho)
+                    CK(cudaMemcpyAsync(rho + xoff + o, stage + o, cc * sizeof(double), cudaMemcpyDeviceToHost,
+                                       c->copy_stream));
+                if (u)
+                    CK(cudaMemcpyAsync(u + 3 * (xoff + o), stage + cells + 3 * o, 3 * cc * sizeof(double),
+                                       cudaMemcpyDeviceToHost, c->copy_stream));
+            }
+            // later work on the context stream (and moments_status's sync) follows the copies
+            CK(cudaEventRecord(c->chunk_events.back(), c->copy_stream));
+            CK(cudaStreamWaitEvent(c->stream, c->chunk_events.back(), 0));
         } else {
             CK(launch_k3_moments<T>(A, P, 0, s.g.nxl, rho ? rho + xoff : nullptr, u ? u + 3 * xoff : nullptr,
                                     c->stream));
@@ -1269,6 +1286,12 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         c->overlap = e ? e[0] == '1' : o.comm == LBM_COMM_NCCL;
         const char* f = getenv("LBM_FUSED_HALO");
         c->fused_halo = !(f && f[0] == '0');
+        if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(c, LBM_ECUDA, "copy stream"));
+        c->chunk_events.resize(9);  // 8 x chunks + the copy stream's completion
+        for (cudaEvent_t& ev : c->chunk_events)
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+                return bail(fail(c, LBM_ECUDA, "read-back events"));
     }
     if (o.comm == LBM_COMM_NCCL) {
         if (!nccl_load()) return bail(fail(c, LBM_ENCCL, "cannot load libnccl.so.2"));
@@ -1303,6 +1326,12 @@ void lbm_destroy(lbm_ctx* c) {
         cudaStreamDestroy(c->comm_stream);
     }
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+    for (cudaEvent_t ev : c->chunk_events)
+        if (ev) cudaEventDestroy(ev);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamDestroy(c->copy_stream);
+    }
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
