@@ -221,7 +221,10 @@ __device__ __forceinline__ long long k0_wcell(const SlabGeom& g, int wx0, int tx
 // cell, either may be null); IMPORT = true: f(t0) given, canonical doubles
 // src[19][wn][ny][nz] (set_populations without a second lattice copy).
 // Planes [xbeg, xbeg + gridDim.z) of the slab.
-template <typename T, int BC, bool IMPORT>
+// RESTU (u == null): every neighbour is at rest, feq_j = w_j rho -- the
+// value feq_dir computes for u = 0 (common = A exactly), without its
+// arithmetic.
+template <typename T, int BC, bool IMPORT, bool RESTU = false>
 __global__ void __launch_bounds__(256) k0_init_pull(const double* __restrict__ rho, const double* __restrict__ u,
                                                    const double* __restrict__ src, long long cstride,
                                                    T* __restrict__ A, StepParams<T> P, int xbeg, int wx0) {
@@ -268,6 +271,9 @@ __global__ void __launch_bounds__(256) k0_init_pull(const double* __restrict__ r
                 const long long t = k0_wcell(g, wx0, tx, ty, tz);
                 if constexpr (IMPORT) {
                     v = T(src[(long long)j * cstride + t]);
+                } else if constexpr (RESTU) {
+                    const T Wa = (rho ? T(rho[t]) : T(1)) * T(1.0 / 18.0);
+                    v = can_axis(j <= 9 ? j : j - 9) ? Wa : T(0.5) * Wa;
                 } else {
                     T rn, uxn, uyn, uzn;
                     k0_load<T>(rho, u, t, rn, uxn, uyn, uzn);
@@ -400,13 +406,15 @@ cudaError_t launch_k0_init_pull(const double* rho, const double* u, const double
     if (nxc <= 0) return cudaSuccess;
     const long long cstride = (long long)wn * g.ny * g.nz;
     const dim3 grid = cell_grid(g.nz, g.ny, nxc);
-#define LBM_K0P(BC, IMP) k0_init_pull<T, BC, IMP><<<grid, kBlock, 0, s>>>(rho, u, src, cstride, A, P, xbeg, wx0)
+#define LBM_K0P(BC, IMP, R) k0_init_pull<T, BC, IMP, R><<<grid, kBlock, 0, s>>>(rho, u, src, cstride, A, P, xbeg, wx0)
     if (g.bc == BC_PERIODIC) {
-        if (src) LBM_K0P(BC_PERIODIC, true);
-        else LBM_K0P(BC_PERIODIC, false);
+        if (src) LBM_K0P(BC_PERIODIC, true, false);
+        else if (u) LBM_K0P(BC_PERIODIC, false, false);
+        else LBM_K0P(BC_PERIODIC, false, true);
     } else {
-        if (src) LBM_K0P(BC_CAVITY, true);
-        else LBM_K0P(BC_CAVITY, false);
+        if (src) LBM_K0P(BC_CAVITY, true, false);
+        else if (u) LBM_K0P(BC_CAVITY, false, false);
+        else LBM_K0P(BC_CAVITY, false, true);
     }
 #undef LBM_K0P
     return cudaGetLastError();
