@@ -86,7 +86,9 @@ typedef enum {
  * odd remainder uses K1.  K2_REG: force the cp.async-staged, warp-specialised
  * variant (kept for A/B measurement; needs 19*ny*nz_pitch*sizeof(T) < 2^30).
  * AUTO = K2, falling back to K1 pairs where no two-step variant fits; an
- * explicit K2/K2_REG on such a slab gives EINVAL from lbm_step.  Results are
+ * explicit K2/K2_REG on such a slab gives EINVAL from lbm_step.  AUTO also
+ * switches to the single-copy K2_SC storage (below) when two lattice copies
+ * do not fit the device's free memory at create but one does.  Results are
  * bitwise identical whichever kernel runs. */
 typedef enum {
     LBM_KERNEL_AUTO = 0,

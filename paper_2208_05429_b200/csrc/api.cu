@@ -1201,6 +1201,29 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     c->x0_proc = o.rank * c->nxl_proc;
     const int sw = o.local_slabs;
     c->slabs.resize(sw);
+    // AUTO: two lattice copies (K2) unless they do not fit the device's free
+    // memory while the single-copy ring does -- then K2_SC (the paper's point
+    // of one copy: larger domains per device).  LBM_MEM_LIMIT_BYTES caps the
+    // free memory considered (tests).
+    bool use_sc = o.kernel == LBM_KERNEL_K2_SC;
+    if (o.kernel == LBM_KERNEL_AUTO) {
+        size_t freeb = 0, totalb = 0;
+        if (cudaMemGetInfo(&freeb, &totalb) != cudaSuccess) {
+            cudaGetLastError();
+            freeb = size_t(-1);
+        }
+        if (const char* e = getenv("LBM_MEM_LIMIT_BYTES")) freeb = std::min(freeb, size_t(atoll(e)));
+        const size_t es_ = dt == LBM_F64 ? 8 : 4;
+        const size_t plane_x = size_t(kQ) * ny * size_t(round_up(nz, int(32 / es_))) * es_;
+        const size_t gap = size_t(dt == LBM_F64 ? k2_sc_gap<double>() : k2_sc_gap<float>());
+        const size_t two = size_t(sw) * 2 * (size_t(nxl) + 4) * plane_x;
+        const size_t lattice = (size_t(nxl) + 4) * plane_x;
+        const size_t stage =
+            std::max({size_t(3) * kQ * ny * nz * sizeof(double), size_t(64) << 20, lattice / 16});
+        const size_t one = size_t(sw) * (size_t(nxl) + 4 + gap) * plane_x + stage;
+        const size_t margin = size_t(256) << 20;
+        if (two + margin > freeb && one + margin <= freeb) use_sc = true;
+    }
     for (int j = 0; j < sw; ++j) {
         Slab& s = c->slabs[j];
         const int grank = o.rank * sw + j;  // global slab index
@@ -1216,12 +1239,17 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         s.g.bc = o.bc;
         s.g.poff = 0;
         s.g.pmod = nxl + 4;
-        if (o.kernel == LBM_KERNEL_K2_SC) {
+        if (use_sc) {
             c->sc = true;
             c->sc_gap = dt == LBM_F64 ? k2_sc_gap<double>() : k2_sc_gap<float>();
             s.g.pmod = nxl + 4 + c->sc_gap;
             const bool ok = dt == LBM_F64 ? k2_supported<double>(s.g) : k2_supported<float>(s.g);
-            if (!ok) return bail(fail(c, LBM_EINVAL, "kernel K2_SC: the TMA descriptor cannot describe this slab"));
+            if (!ok && o.kernel == LBM_KERNEL_K2_SC)
+                return bail(fail(c, LBM_EINVAL, "kernel K2_SC: the TMA descriptor cannot describe this slab"));
+            if (!ok) {  // AUTO: keep two copies (the allocation may then fail: ENOMEM)
+                use_sc = c->sc = false;
+                s.g.pmod = nxl + 4;
+            }
         }
         // cavity chain: only the outer faces of the first and last slab are walls
         s.g.left_wall = (o.bc == LBM_BC_CAVITY && grank == 0);

@@ -239,3 +239,27 @@ def test_single_copy_full_size_soak_bitwise(dtype):
     for a, b in zip(p1, p2):
         assert np.array_equal(a, b)
     assert np.all(np.isfinite(u2))
+
+
+def test_auto_switches_to_single_copy_when_two_copies_do_not_fit(monkeypatch):
+    """AUTO with a device that cannot hold two lattice copies but can hold
+    the ring (LBM_MEM_LIMIT_BYTES caps the free memory it considers): the
+    context takes the single-copy storage -- about half the memory -- and
+    gives the two-buffer bits."""
+    dims = (1024, 64, 64)  # two copies 1.28 GB; the ring + staging 0.75 GB
+    f0 = li.random_populations(97, *dims)
+    outs, used = [], []
+    for limit in (None, "1200000000"):
+        if limit:
+            monkeypatch.setenv("LBM_MEM_LIMIT_BYTES", limit)
+        torch.cuda.synchronize()
+        free0, _ = torch.cuda.mem_get_info()
+        with lbm.Lattice(*dims, 0.6, LID, "f64") as lat:
+            free1, _ = torch.cuda.mem_get_info()
+            lat.set_populations(f0)
+            lat.step(5)
+            outs.append(lat.populations())
+        used.append(free0 - free1)
+        monkeypatch.delenv("LBM_MEM_LIMIT_BYTES", raising=False)
+    assert np.array_equal(outs[0], outs[1])
+    assert used[0] > 1.2e9 and used[1] < 0.85e9, used
