@@ -148,9 +148,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// periodic index wrap: one period away without a division (every wrapped
+// K2 source, except in domains narrower than a tile: the % path)
 __device__ __forceinline__ int wrapi(int v, int n) {
-    v %= n;
-    return v < 0 ? v + n : v;
+    int w = v < 0 ? v + n : (v >= n ? v - n : v);
+    if (w < 0 || w >= n) {
+        w = v % n;
+        if (w < 0) w += n;
+    }
+    return w;
 }
 
 }  // namespace
