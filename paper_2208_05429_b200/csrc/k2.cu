@@ -380,11 +380,10 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         const bool rwall = BC == BC_CAVITY && p == g.nxl - 1 && g.right_wall;
         // Periodic edge tiles: sources that wrap (outside [0,ny) x [0,nz); the
         // TMA zero-filled them) are loaded per thread from the wrapped cell
-        // (no CTA-wide fix-up pass: measured +9% over one).  fp64 issues them
-        // before the stage wait so their latency overlaps it (config 3 26.7k
-        // -> 28.0k); fp32 after the stage read (early: 41.5k -> 40.8k).  With
-        // zpre the z-wrap lanes take theirs from the prefetch instead.
-        constexpr bool kEarlyWrap = sizeof(T) == 8;
+        // after the stage read (no CTA-wide fix-up pass: measured +9% over
+        // one; issuing them before the stage wait paid only while the wrap
+        // used an integer division).  With zpre the z-wrap lanes take theirs
+        // from the prefetch instead.
         T fs[kQ];
         const bool wdir = BC == BC_PERIODIC && has1 && (edge_y || (edge_z && !zpre)) && act1;
         auto wraps = [&](int cy, int cz) {
@@ -404,7 +403,6 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 });
             }
         };
-        if constexpr (BC == BC_PERIODIC && kEarlyWrap) load_wrapped();
         if (has1) {
             mbar_wait(&bar[s], uint32_t(c >> 1) & 1u);
         }
@@ -420,10 +418,9 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 static_for<0, kQ>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
                     constexpr int i = slot_dir(k);
-                    if (BC == BC_PERIODIC && kEarlyWrap && wdir && wraps(can_cy(i), can_cz(i))) return;
                     fs[i] = sp[k * C::BOXE - can_cz(i)];
                 });
-                if constexpr (BC == BC_PERIODIC && !kEarlyWrap) load_wrapped();
+                if constexpr (BC == BC_PERIODIC) load_wrapped();
                 if constexpr (BC == BC_PERIODIC) {
                     // z-wrap lanes: their prefetched wrapped values
                     if constexpr (kZPre) {
