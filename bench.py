@@ -154,8 +154,10 @@ def run_reference(args, cfg):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1000 * secs / max(1, args.steps), 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "nx": cfg.nx, "ny": cfg.ny, "nz": cfg.nz,
-                   "bc": "periodic" if cfg.bc else "cavity", "tau": cfg.tau, "u_lid": list(cfg.u_lid)},
+        "config": {"workload": f"{cfg.name} (CPU oracle timed on a sample of it)", "nx": cfg.nx, "ny": cfg.ny,
+                   "nz": cfg.nz, "bc": "periodic" if cfg.bc else "cavity", "tau": cfg.tau,
+                   "u_lid": list(cfg.u_lid), "sample": sample,
+                   "ms_per_step": "time of one bench step's sample, not of a whole job"},
         "cpu_baseline": {"value": round(value, 3), "unit": "MLUPS", "cores": threads, "kind": "oracle",
                          "sample": sample, "cpu": model, "host_cpus": ncpu},
         "e2e": {"value": round(value, 3), "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -173,9 +175,11 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "k1", "k2", "k2reg", "aa", "k2sc"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "k1", "k2", "aa", "k2sc"])
     ap.add_argument("--lbm-steps", type=int, default=None, help="time steps per job (default: the config's)")
     ap.add_argument("--dims", default=None, help="override NX,NY,NZ (profiling runs only)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling (BASELINE.json:11): 128 x 512 x 512 cells of config 5 per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -188,6 +192,10 @@ def main():
     if args.dims:
         nx, ny, nz = (int(v) for v in args.dims.split(","))
         cfg = cfg.with_dims(nx, ny, nz)
+    if args.weak:
+        if args.config != 5:
+            ap.error("--weak is config 5's weak-scaling series (128x512x512 per GPU)")
+        cfg = cfg.with_dims(128 * max(1, int(os.environ.get("WORLD_SIZE", "1"))), cfg.ny, cfg.nz)
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -210,7 +218,7 @@ def main():
     x0 = rank * nxl
     cells_local = nxl * cfg.ny * cfg.nz
     stream = torch.cuda.Stream(device=dev)
-    kernel = {"auto": lbm.LBM_KERNEL_AUTO, "k1": lbm.LBM_KERNEL_K1, "k2": lbm.LBM_KERNEL_K2, "k2reg": lbm.LBM_KERNEL_K2_REG,
+    kernel = {"auto": lbm.LBM_KERNEL_AUTO, "k1": lbm.LBM_KERNEL_K1, "k2": lbm.LBM_KERNEL_K2,
               "aa": lbm.LBM_KERNEL_AA, "k2sc": lbm.LBM_KERNEL_K2_SC}[args.kernel]
 
     nccl_id = None
@@ -349,8 +357,8 @@ def main():
         line = {
             "metric": "MLUPS", "value": round(value, 3), "unit": "MLUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
-            "data": "synthetic",
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": cfg.name, "nx": cfg.nx, "ny": cfg.ny, "nz": cfg.nz,
                        "bc": "periodic" if cfg.bc else "cavity", "tau": cfg.tau, "u_lid": list(cfg.u_lid),
                        "lbm_steps_per_job": cfg.steps, "job": "init_equilibrium + lbm_step(n) + macroscopic",

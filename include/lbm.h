@@ -39,9 +39,29 @@
  *              lbm_last_error / lbm_destroy returns LBM_ESTATE.  Errors of
  *              asynchronous work surface at the next blocking call.
  *              LBM_ENUMERIC from a blocking read-back of degenerate or
- *              non-finite moments (the context stays usable).
+ *              non-finite moments (the context stays usable).  An input
+ *              rejected by lbm_init_equilibrium / lbm_set_populations
+ *              (EINVAL) may already have overwritten part of the state: it
+ *              is then undefined, and lbm_step / the read-backs return
+ *              LBM_ESTATE until a successful init.
+ *  NCCL        with comm == NCCL every call that touches the state is
+ *              COLLECTIVE: all ranks make the same sequence of
+ *              lbm_init_equilibrium(_device), lbm_set_populations,
+ *              lbm_step, lbm_macroscopic(_device) and
+ *              lbm_get_populations(_box) calls (read-backs exchange stale
+ *              ghost planes first -- also for an empty box).  Input
+ *              validation is agreed across ranks: if one rank rejects its
+ *              input, every rank returns EINVAL before any exchange.
+ *              Failure detection: blocking calls poll the communicator; an
+ *              asynchronous NCCL error, or no sweep completing for
+ *              LBM_NCCL_TIMEOUT_S seconds (default 120: a lost or stalled
+ *              peer), aborts the communicator and returns LBM_ENCCL (the
+ *              context is poisoned).  lbm_create_ex's AUTO storage choice
+ *              is made on the smallest free memory of all ranks, so every
+ *              rank picks the same storage.
  *  Threads     a context is not thread-safe; distinct contexts are
- *              independent.
+ *              independent.  Every call leaves the calling thread's current
+ *              CUDA device as it found it.
  */
 #ifndef LBM_B200_H
 #define LBM_B200_H
@@ -82,11 +102,11 @@ typedef enum {
  * (Alg. 1's loop fusion).  K2: two steps per HBM pass, temporally blocked
  * on chip (Alg. 2's two-step merge): TMA-staged shared-memory tiles where the
  * TMA descriptor can describe the slab (z pitch a multiple of 16 bytes,
- * (nx_local+4)*19 < 2^31), otherwise the cp.async-staged variant K2_REG; an
- * odd remainder uses K1.  K2_REG: force the cp.async-staged, warp-specialised
- * variant (kept for A/B measurement; needs 19*ny*nz_pitch*sizeof(T) < 2^30).
- * AUTO = K2, falling back to K1 pairs where no two-step variant fits; an
- * explicit K2/K2_REG on such a slab gives EINVAL from lbm_step.  AUTO also
+ * (nx_local+4)*19 < 2^31); an odd remainder uses K1.  K2_REG (value 3) is
+ * reserved: the cp.async-staged variant it named measured slower than K2
+ * wherever K2 applies and was removed -- lbm_create_ex rejects it (EINVAL).
+ * AUTO = K2, falling back to K1 pairs where the descriptor cannot describe
+ * the slab; an explicit K2 on such a slab gives EINVAL from lbm_step.  AUTO also
  * switches to the single-copy K2_SC storage (below) when two lattice copies
  * do not fit the device's free memory at create but one does.  Results are
  * bitwise identical whichever kernel runs. */

@@ -137,6 +137,14 @@ def run(f, bc: int, tau: float, u_lid=(0.0, 0.0, 0.0), n: int = 1) -> np.ndarray
     return g
 
 
+def run_inplace(f, bc: int, tau: float, u_lid=(0.0, 0.0, 0.0), n: int = 1) -> None:
+    """``run`` without the copy: advances the C-contiguous float64 f in place
+    (full-size golden runs hold two lattices, not three)."""
+    _, nx, ny, nz = f.shape
+    if lib().oracle_run(nx, ny, nz, int(bc), float(tau), _p(_vec3(u_lid)), int(n), _p(f)):
+        raise MemoryError("oracle_run: allocation failed")
+
+
 def step_box(f_box, dims, origin, bc: int, tau: float, u_lid=(0.0, 0.0, 0.0)) -> np.ndarray:
     """One step on a sub-box of a global domain; unknown pulls become NaN."""
     f_box = np.ascontiguousarray(f_box, dtype=np.float64)

@@ -141,16 +141,11 @@ void oracle_init_equilibrium(int nx, int ny, int nz, const double *rho,
 
 static int wrap(int s, int n) { return ((s % n) + n) % n; }
 
-void oracle_step_box(int nx, int ny, int nz, int bc, double tau,
-                     const double u_lid[3], int bx, int by, int bz,
-                     int lx, int ly, int lz, const double *f_in, double *f_out) {
-    init_tables();
-    const double omega = 1.0 / tau;
-    const double rho_w = 1.0;
-    size_t ncell = (size_t)lx * ly * lz;
-    double *fstar = (double *)malloc(sizeof(double) * 19 * ncell);
-
-    /* 1. collide every cell of the box */
+/* Step part 1: BGK-collide every cell of an
+ * lx*ly*lz array, f_in -> fstar.  f_in == fstar is allowed: each cell reads
+ * its 19 values before writing them. */
+static void collide_all(int lx, int ly, int lz, double omega,
+                        const double *f_in, double *fstar) {
 #pragma omp parallel for schedule(static) num_threads(oracle_get_threads())
     for (int x = 0; x < lx; x++)
         for (int y = 0; y < ly; y++)
@@ -160,8 +155,14 @@ void oracle_step_box(int nx, int ny, int nz, int bc, double tau,
                 oracle_collide(f, omega, out);
                 for (int i = 0; i < 19; i++) fstar[idx(i, x, y, z, lx, ly, lz)] = out[i];
             }
+}
 
-    /* 2. pull-stream with the boundary rules */
+/* Step part 2: pull-stream the post-collision box
+ * fstar into f_out with the boundary rules of the global domain. */
+static void stream_all(int nx, int ny, int nz, int bc, const double u_lid[3],
+                       int bx, int by, int bz, int lx, int ly, int lz,
+                       const double *fstar, double *f_out) {
+    const double rho_w = 1.0;
 #pragma omp parallel for schedule(static) num_threads(oracle_get_threads())
     for (int x = 0; x < lx; x++)
         for (int y = 0; y < ly; y++)
@@ -192,6 +193,16 @@ void oracle_step_box(int nx, int ny, int nz, int bc, double tau,
                     f_out[idx(i, x, y, z, lx, ly, lz)] = v;
                 }
             }
+}
+
+void oracle_step_box(int nx, int ny, int nz, int bc, double tau,
+                     const double u_lid[3], int bx, int by, int bz,
+                     int lx, int ly, int lz, const double *f_in, double *f_out) {
+    init_tables();
+    size_t ncell = (size_t)lx * ly * lz;
+    double *fstar = (double *)malloc(sizeof(double) * 19 * ncell);
+    collide_all(lx, ly, lz, 1.0 / tau, f_in, fstar);
+    stream_all(nx, ny, nz, bc, u_lid, bx, by, bz, lx, ly, lz, fstar, f_out);
     free(fstar);
 }
 
@@ -200,15 +211,24 @@ void oracle_step(int nx, int ny, int nz, int bc, double tau,
     oracle_step_box(nx, ny, nz, bc, tau, u_lid, 0, 0, 0, nx, ny, nz, f_in, f_out);
 }
 
+/* The same two parts per step with two lattices only (collide in place,
+ * pull into the other lattice, swap), so a full-size run holds 2 copies. */
 int oracle_run(int nx, int ny, int nz, int bc, double tau,
                const double u_lid[3], long n, double *f) {
+    init_tables();
     size_t len = (size_t)19 * nx * ny * nz;
+    if (n <= 0) return 0;
     double *g = (double *)malloc(sizeof(double) * len);
     if (!g) return 1;
+    double *a = f, *b = g;
     for (long t = 0; t < n; t++) {
-        oracle_step(nx, ny, nz, bc, tau, u_lid, f, g);
-        memcpy(f, g, sizeof(double) * len);
+        collide_all(nx, ny, nz, 1.0 / tau, a, a);
+        stream_all(nx, ny, nz, bc, u_lid, 0, 0, 0, nx, ny, nz, a, b);
+        double *tmp = a;
+        a = b;
+        b = tmp;
     }
+    if (a != f) memcpy(f, a, sizeof(double) * len);
     free(g);
     return 0;
 }

@@ -11,7 +11,10 @@
 // (PAPER.md:747-749).
 #include <dlfcn.h>
 
+#include <unistd.h>
+
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdarg>
@@ -42,6 +45,10 @@ struct NcclApi {
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 NcclApi g_nccl;
 
@@ -60,13 +67,33 @@ bool nccl_load() {
     LOADSYM(Send, "ncclSend");
     LOADSYM(Recv, "ncclRecv");
     LOADSYM(GetErrorString, "ncclGetErrorString");
+    LOADSYM(AllReduce, "ncclAllReduce");
+    LOADSYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    LOADSYM(CommAbort, "ncclCommAbort");
 #undef LOADSYM
     g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.GroupStart &&
-                g_nccl.GroupEnd && g_nccl.Send && g_nccl.Recv;
+                g_nccl.GroupEnd && g_nccl.Send && g_nccl.Recv && g_nccl.AllReduce && g_nccl.CommGetAsyncError &&
+                g_nccl.CommAbort;
     return g_nccl.ok;
 }
 
 thread_local std::string t_last_error;
+
+// Every ABI call leaves the calling thread's current device as it found it
+// (the library switches to the context's device internally).
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
 }  // namespace
 
 // ------------------------------------------------------------- context ---
@@ -110,6 +137,12 @@ struct lbm_ctx {
     cudaStream_t copy_stream = nullptr;
     std::vector<cudaEvent_t> chunk_events;
     ncclComm_t comm = nullptr;
+    // NCCL watchdog (wait_stream): a progress event per sweep; a blocking
+    // call fails with ENCCL on an asynchronous NCCL error or when no sweep
+    // has completed for nccl_timeout_s seconds (a lost or stalled peer)
+    std::vector<cudaEvent_t> progress;
+    long long progress_issued = 0, progress_done = 0;
+    double nccl_timeout_s = 120.0;
     size_t esize = 8;
     int* d_flag = nullptr;
     // diagnostics
@@ -155,6 +188,85 @@ lbm_status fail(lbm_ctx* c, lbm_status st, const char* fmt, ...) {
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
+// ------------------------------------------------------ NCCL watchdog ----
+// Failure detection for NCCL contexts (a lost or stalled peer must not hang
+// the caller forever).  Every sweep records a progress event on the context
+// stream; a blocking wait polls the stream, ncclCommGetAsyncError, and the
+// progress events: an asynchronous NCCL error, or no sweep completing for
+// nccl_timeout_s seconds (LBM_NCCL_TIMEOUT_S, default 120), aborts the
+// communicator (its kernels stop) and fails with ENCCL; the context is then
+// poisoned.  Without NCCL a wait is a plain stream synchronize.
+lbm_status nccl_abort(lbm_ctx* c, const char* why) {
+    if (c->comm && g_nccl.CommAbort) g_nccl.CommAbort(c->comm);
+    c->comm = nullptr;
+    return fail(c, LBM_ENCCL, "%s (communicator aborted)", why);
+}
+
+lbm_status record_progress(lbm_ctx* c) {
+    if (!c->comm || c->progress.empty()) return LBM_OK;
+    CK(cudaEventRecord(c->progress[size_t(c->progress_issued % (long long)c->progress.size())], c->stream));
+    c->progress_issued++;
+    return LBM_OK;
+}
+
+lbm_status wait_stream(lbm_ctx* c, cudaStream_t st) {
+    if (!c->comm) {
+        CK(cudaStreamSynchronize(st));
+        return LBM_OK;
+    }
+    using clk = std::chrono::steady_clock;
+    auto last = clk::now();
+    for (unsigned spin = 0;; ++spin) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e == cudaSuccess) {
+            c->progress_done = c->progress_issued;
+            return LBM_OK;
+        }
+        if (e != cudaErrorNotReady) return fail(c, LBM_ECUDA, "stream wait: %s", cudaGetErrorString(e));
+        ncclResult_t ar = ncclSuccess;
+        if (g_nccl.CommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+            char why[256];
+            snprintf(why, sizeof why, "NCCL asynchronous error: %s",
+                     g_nccl.GetErrorString ? g_nccl.GetErrorString(ar) : "?");
+            return nccl_abort(c, why);
+        }
+        // progress: the oldest sweep event still held in the ring
+        const long long n = (long long)c->progress.size();
+        if (c->progress_done < c->progress_issued - n) c->progress_done = c->progress_issued - n;
+        while (c->progress_done < c->progress_issued) {
+            const cudaError_t q = cudaEventQuery(c->progress[size_t(c->progress_done % n)]);
+            if (q == cudaErrorNotReady) break;
+            if (q != cudaSuccess) return fail(c, LBM_ECUDA, "progress event: %s", cudaGetErrorString(q));
+            c->progress_done++;
+            last = clk::now();
+        }
+        if (std::chrono::duration<double>(clk::now() - last).count() > c->nccl_timeout_s) {
+            char why[256];
+            snprintf(why, sizeof why, "no progress for %.0f s: a peer rank is lost or stalled (LBM_NCCL_TIMEOUT_S)",
+                     c->nccl_timeout_s);
+            return nccl_abort(c, why);
+        }
+        if (spin > 64) usleep(spin > 4096 ? 1000 : 50);
+    }
+}
+
+// Input validation that every rank agrees on: under NCCL the per-rank
+// verdicts are max-reduced before anything collective follows, so a rank
+// that rejects its input does not leave its peers blocked in an exchange.
+lbm_status agree_valid(lbm_ctx* c, int bad, const char* why) {
+    if (c->comm) {
+        int* d = c->d_flag;
+        CK(cudaMemcpyAsync(d, &bad, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        CKN(g_nccl.AllReduce(d, d, 1, ncclInt32, ncclMax, c->comm, c->stream));
+        CK(cudaMemcpyAsync(&bad, d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        lbm_status st = wait_stream(c, c->stream);
+        if (st != LBM_OK) return st;
+        if (bad && !why) why = "another rank rejected its input";
+    }
+    if (bad) return fail(c, LBM_EINVAL, "%s (state is now undefined: initialise again)", why ? why : "invalid input");
+    return LBM_OK;
+}
+
 void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world, int nxl, int x0,
                lbm_halo_plan* p) {
     memset(p, 0, sizeof *p);
@@ -162,6 +274,12 @@ void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world
     p->x0 = x0;
     p->nz_pitch = round_up(nz, int(32 / esize));  // rows start on 32 B sectors
     p->plane_q = (long long)ny * p->nz_pitch;
+    if (const char* e = getenv("LBM_EXP_PAD")) {  // EXPERIMENT (temporary): "<z elems>,<y rows>"
+        int zp = 0, yp = 0;
+        sscanf(e, "%d,%d", &zp, &yp);
+        p->nz_pitch += zp;
+        p->plane_q = (long long)(ny + yp) * p->nz_pitch;
+    }
     p->plane_x = (long long)kQ * p->plane_q;
     p->buffer_elems = (long long)(nxl + 4) * p->plane_x;
     if (bc == LBM_BC_PERIODIC) {
@@ -465,6 +583,7 @@ lbm_status run_steps_aa(lbm_ctx* c, long n) {
             if (st != LBM_OK) return st;
         }
         st = prof_end(c, slot, updates);
+        if (st == LBM_OK) st = record_progress(c);
         if (st != LBM_OK) return st;
         c->aa_odd = !c->aa_odd;
         c->ghosts_valid = false;
@@ -501,6 +620,7 @@ lbm_status run_steps_sc(lbm_ctx* c, long n) {
             s.g.poff = out_poff;
         }
         st = prof_end(c, slot, updates);
+        if (st == LBM_OK) st = record_progress(c);
         if (st != LBM_OK) return st;
         c->ghosts_valid = false;
         c->t += nsteps;
@@ -514,8 +634,10 @@ lbm_status run_steps_sc(lbm_ctx* c, long n) {
 // place (launch_k1_sc with unstream, shifting the window like a K1 step).
 template <typename T>
 lbm_status sc_finish_canonical(lbm_ctx* c) {
+    lbm_status st = agree_valid(c, 0, nullptr);  // NCCL: every rank's inputs passed
+    if (st != LBM_OK) return st;
     c->ghosts_valid = false;
-    lbm_status st = ensure_ghosts(c);
+    st = ensure_ghosts(c);
     if (st != LBM_OK) return st;
     for (Slab& s : c->slabs) {
         const StepParams<T> P = make_params<T>(c, s);
@@ -537,16 +659,12 @@ lbm_status run_steps(lbm_ctx* c, long n) {
     if (c->aa) return run_steps_aa<T>(c, n);
     if (c->sc) return run_steps_sc<T>(c, n);
     // AUTO and K2: the TMA-staged two-step sweep (k2.cu) where the TMA
-    // descriptor can describe the slab, else the cp.async-staged one (K2R,
-    // k2r.cu); K2_REG forces K2R.  AUTO falls back to K1 pairs when neither
-    // fits; an explicit two-step request then fails.
-    const bool reg_only = c->opts.kernel == LBM_KERNEL_K2_REG;
-    bool tma = !reg_only && c->opts.kernel != LBM_KERNEL_K1;
+    // descriptor can describe the slab; AUTO falls back to K1 pairs where it
+    // cannot, an explicit K2 request then fails.
+    bool tma = c->opts.kernel != LBM_KERNEL_K1;
     for (const Slab& s : c->slabs) tma = tma && k2_supported<T>(s.g);
-    bool use_k2 = c->opts.kernel != LBM_KERNEL_K1;
-    if (!tma)
-        for (const Slab& s : c->slabs) use_k2 = use_k2 && k2r_supported<T>(s.g);
-    if (c->opts.kernel >= LBM_KERNEL_K2 && !use_k2 && n >= 2)
+    const bool use_k2 = tma;
+    if (c->opts.kernel == LBM_KERNEL_K2 && !use_k2 && n >= 2)
         return fail(c, LBM_EINVAL, "two-step kernel requested but not supported for this geometry");
     // Fused halo (k2.cu): TMA K2 sweeps store the neighbours' ghost planes
     // themselves when the neighbours' buffers are addressable here (one
@@ -556,15 +674,15 @@ lbm_status run_steps(lbm_ctx* c, long n) {
     while (n > 0) {
         const int nsteps = (use_k2 && n >= 2) ? 2 : 1;
         const bool fused = fuse && nsteps == 2;
-        auto launch = [&](Slab& s, int xbeg, int nxs) -> cudaError_t {
+        // planes [xbeg, xbeg + nxs) (and [xbeg2, xbeg2 + nxs) in the same grid)
+        auto launch = [&](Slab& s, int xbeg, int nxs, int xbeg2 = 0, int nxs2 = 0) -> cudaError_t {
             const StepParams<T> P = make_params<T>(c, s);
             const T* A = static_cast<const T*>(s.buf[c->cur]);
             T* B = static_cast<T*>(s.buf[c->cur ^ 1]);
             T* hl = fused && s.left >= 0 ? static_cast<T*>(c->slabs[s.left].buf[c->cur ^ 1]) : nullptr;
             T* hr = fused && s.right >= 0 ? static_cast<T*>(c->slabs[s.right].buf[c->cur ^ 1]) : nullptr;
-            return nsteps == 1 ? launch_k1<T>(A, B, P, xbeg, nxs, c->stream)
-                   : tma       ? launch_k2<T>(A, B, P, xbeg, nxs, c->stream, 0, nullptr, hl, hr)
-                               : launch_k2r<T>(A, B, P, xbeg, nxs, c->stream);
+            return nsteps == 1 ? launch_k1<T>(A, B, P, xbeg, nxs, c->stream, xbeg2, nxs2)
+                               : launch_k2<T>(A, B, P, xbeg, nxs, c->stream, 0, nullptr, hl, hr, xbeg2, nxs2);
         };
         // Planes [h, nxl-h) read no ghost plane (h = the sweep's step count),
         // so with neighbours the exchange runs on the comm stream while they
@@ -597,13 +715,15 @@ lbm_status run_steps(lbm_ctx* c, long n) {
         if (split) {
             CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
             for (Slab& s : c->slabs) {
-                cudaError_t e = launch(s, 0, h);
-                if (e == cudaSuccess) e = launch(s, s.g.nxl - h, h);
+                // both h-plane edge ranges in ONE grid (a 2-plane range alone
+                // is a fraction of a wave of the machine)
+                cudaError_t e = launch(s, 0, h, s.g.nxl - h, h);
                 if (e != cudaSuccess) return fail(c, LBM_ECUDA, "edge sweep launch failed: %s", cudaGetErrorString(e));
-                c->launches += 2;
+                c->launches += 1;
             }
         }
         pst = prof_end(c, slot, updates);
+        if (pst == LBM_OK) pst = record_progress(c);
         if (pst != LBM_OK) return pst;
         (nsteps == 2 ? c->k2_launches : c->k1_launches) += (long long)c->slabs.size();
         c->cur ^= 1;
@@ -633,13 +753,14 @@ lbm_status validate_device(lbm_ctx* c, const double* v, long long n, bool positi
         c->launches++;
     }
     CK(cudaMemcpyAsync(out, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    return LBM_OK;
+    return wait_stream(c, c->stream);
 }
 
 // f(t0) canonical in buffer `which` of every slab (own planes) -> state.
 template <typename T>
 lbm_status finish_init(lbm_ctx* c, int canon) {
+    lbm_status vst = agree_valid(c, 0, nullptr);  // NCCL: every rank's inputs passed
+    if (vst != LBM_OK) return vst;
     if (c->aa) {  // canonical f(t0) in buf[0] IS the at-rest AA state
         c->cur = 0;
         c->aa_odd = false;
@@ -698,9 +819,9 @@ lbm_status init_eq_aa(lbm_ctx* c, const double* rho, const double* u, bool host)
             int flag = 0;
             lbm_status st;
             if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
-            if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+            if (flag) return agree_valid(c, 1, "rho must be finite and > 0");
             if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
-            if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+            if (flag) return agree_valid(c, 1, "u must be finite");
             CK(launch_k0_equilibrium<T>(dr, du, F, s.g, c->stream, xb, nxc));
             c->launches++;
         }
@@ -780,9 +901,9 @@ lbm_status init_eq_sc(lbm_ctx* c, const double* rho, const double* u, bool host)
                 int flag = 0;
                 lbm_status st;
                 if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
-                if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+                if (flag) return agree_valid(c, 1, "rho must be finite and > 0");
                 if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
-                if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+                if (flag) return agree_valid(c, 1, "u must be finite");
                 CK(launch_k0_equilibrium<T>(dr, du, F, s.g, c->stream, xb, nxc));
                 c->launches++;
             }
@@ -818,9 +939,9 @@ lbm_status init_eq_sc(lbm_ctx* c, const double* rho, const double* u, bool host)
         }
         int flag = 0;
         if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
-        if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+        if (flag) return agree_valid(c, 1, "rho must be finite and > 0");
         if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
-        if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+        if (flag) return agree_valid(c, 1, "u must be finite");
         CK(launch_k0_init_pull<T>(dr, du, nullptr, F, P, xb, nxc, w.w0, w.wn, c->stream));
         c->launches++;
     }
@@ -847,7 +968,7 @@ lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
                 int flag = 0;
                 lbm_status st = validate_device(c, stage, kQ * ccells, false, &flag);
                 if (st != LBM_OK) return st;
-                if (flag) return fail(c, LBM_EINVAL, "populations must be finite (state is now undefined)");
+                if (flag) return agree_valid(c, 1, "populations must be finite");
                 CK(launch_k0_import<T>(stage, static_cast<T*>(s.buf[0]), s.g, xb, nxc, c->stream));
                 c->launches++;
             }
@@ -870,7 +991,7 @@ lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
         int flag = 0;
         st = validate_device(c, stage, (long long)kQ * w.wn * plane, false, &flag);
         if (st != LBM_OK) return st;
-        if (flag) return fail(c, LBM_EINVAL, "populations must be finite (state is now undefined)");
+        if (flag) return agree_valid(c, 1, "populations must be finite");
         CK(launch_k0_init_pull<T>(nullptr, nullptr, stage, F, P, xb, nxc, w.w0, w.wn, c->stream));
         c->launches++;
     }
@@ -879,6 +1000,9 @@ lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
 
 template <typename T>
 lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
+    // the state is rewritten from here on: invalid until the init completes
+    // (a rejected input leaves it undefined, include/lbm.h)
+    c->initialized = false;
     if (c->aa) return init_eq_aa<T>(c, rho, u, host);
     if (c->sc) return init_eq_sc<T>(c, rho, u, host);
     const long long plane = (long long)c->ny * c->nz;
@@ -903,9 +1027,9 @@ lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
             int flag = 0;
             lbm_status st;
             if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
-            if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+            if (flag) return agree_valid(c, 1, "rho must be finite and > 0");
             if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
-            if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+            if (flag) return agree_valid(c, 1, "u must be finite");
         } else {
             dr = rho ? rho + xoff : nullptr;
             du = u ? u + 3 * xoff : nullptr;
@@ -950,7 +1074,7 @@ lbm_status set_pops(lbm_ctx* c, const double* f) {
             int flag = 0;
             lbm_status st = validate_device(c, stage, kQ * ccells, false, &flag);
             if (st != LBM_OK) return st;
-            if (flag) return fail(c, LBM_EINVAL, "populations must be finite (state is now undefined)");
+            if (flag) return agree_valid(c, 1, "populations must be finite");
             CK(launch_k0_import<T>(stage, static_cast<T*>(s.buf[canon]), s.g, xb, nxc, c->stream));
             c->launches++;
         }
@@ -965,7 +1089,8 @@ lbm_status set_pops(lbm_ctx* c, const double* f) {
 lbm_status moments_status(lbm_ctx* c) {
     int flag = 0;
     CK(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    lbm_status st = wait_stream(c, c->stream);
+    if (st != LBM_OK) return st;
     if (flag & 1) return fail(c, LBM_ENUMERIC, "degenerate moments: rho == 0 in some cell (u undefined there)");
     if (flag & 2) return fail(c, LBM_ENUMERIC, "non-finite moments: the state has diverged");
     return LBM_OK;
@@ -1087,8 +1212,7 @@ lbm_status get_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, d
                                  c->stream));
         }
     }
-    CK(cudaStreamSynchronize(c->stream));
-    return LBM_OK;
+    return wait_stream(c, c->stream);
 }
 
 }  // namespace
@@ -1134,6 +1258,7 @@ lbm_status lbm_create(lbm_ctx** out, int nx, int ny, int nz, double tau, const d
 
 lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, const double u_lid[3], lbm_dtype dt,
                          const lbm_opts* user_opts) {
+    DeviceGuard dg;
     lbm_ctx* c = nullptr;
     if (!out) return fail(c, LBM_EINVAL, "out is NULL");
     *out = nullptr;
@@ -1165,6 +1290,8 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     if (o.comm == LBM_COMM_LOCAL && o.world != 1) return fail(c, LBM_EINVAL, "comm LOCAL needs world == 1");
     if (o.comm < LBM_COMM_NONE || o.comm > LBM_COMM_LOCAL) return fail(c, LBM_EINVAL, "bad comm %d", o.comm);
     if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K2_SC) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    if (o.kernel == LBM_KERNEL_K2_REG)
+        return fail(c, LBM_EINVAL, "kernel K2_REG was removed (slower than K2 wherever K2 applies; DESIGN.md section 5)");
     if (o.kernel == LBM_KERNEL_AA && o.bc == LBM_BC_CAVITY && (o.world > 1 || o.local_slabs > 1) &&
         nx / (o.world * o.local_slabs) < 2)
         return fail(c, LBM_EINVAL, "kernel AA with X-slabs needs >= 2 planes per slab");
@@ -1201,6 +1328,51 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     c->x0_proc = o.rank * c->nxl_proc;
     const int sw = o.local_slabs;
     c->slabs.resize(sw);
+    // scratch word(s): validation flags, NCCL agreement (8 bytes)
+    if (cudaMalloc(&c->d_flag, 16) != cudaSuccess) return bail(fail(c, LBM_ENOMEM, "cudaMalloc flag"));
+    if (o.stream) {
+        c->stream = static_cast<cudaStream_t>(o.stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(c, LBM_ECUDA, "cudaStreamCreate"));
+        c->own_stream = true;
+    }
+    {
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
+            cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+            return bail(fail(c, LBM_ECUDA, "comm stream / events"));
+        // Overlap the exchange with the interior sweep where the exchange
+        // crosses NVLink (NCCL).  On one device (LOCAL slabs, the periodic
+        // wrap) the copies are cheaper than the extra edge launches the split
+        // costs (measured 8 LOCAL slabs: 31.7k MLUPS serial vs 29.9k split),
+        // so there it is off.  LBM_OVERLAP=0/1 forces it (A/B runs, tests).
+        const char* e = getenv("LBM_OVERLAP");
+        c->overlap = e ? e[0] == '1' : o.comm == LBM_COMM_NCCL;
+        const char* f = getenv("LBM_FUSED_HALO");
+        c->fused_halo = !(f && f[0] == '0');
+        if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(c, LBM_ECUDA, "copy stream"));
+        c->chunk_events.resize(9);  // 8 x chunks + the copy stream's completion
+        for (cudaEvent_t& ev : c->chunk_events)
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+                return bail(fail(c, LBM_ECUDA, "read-back events"));
+    }
+    if (o.comm == LBM_COMM_NCCL) {
+        if (!nccl_load()) return bail(fail(c, LBM_ENCCL, "cannot load libnccl.so.2"));
+        ncclUniqueId id;
+        memcpy(&id, o.nccl_id, sizeof id);
+        ncclResult_t r = g_nccl.CommInitRank(&c->comm, o.world, id, o.rank);
+        if (r != ncclSuccess)
+            return bail(fail(c, LBM_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+        if (const char* e = getenv("LBM_NCCL_TIMEOUT_S")) c->nccl_timeout_s = std::max(1.0, atof(e));
+        c->progress.resize(64);
+        for (cudaEvent_t& ev : c->progress)
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+                return bail(fail(c, LBM_ECUDA, "progress events"));
+    }
     // AUTO: two lattice copies (K2) unless they do not fit the device's free
     // memory while the single-copy ring does -- then K2_SC (the paper's point
     // of one copy: larger domains per device).  LBM_MEM_LIMIT_BYTES caps the
@@ -1213,8 +1385,21 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
             freeb = size_t(-1);
         }
         if (const char* e = getenv("LBM_MEM_LIMIT_BYTES")) freeb = std::min(freeb, size_t(atoll(e)));
+        if (c->comm) {
+            // every rank must pick the same storage (the halo parts differ):
+            // decide on the smallest free memory of all ranks
+            unsigned long long fb = freeb;
+            if (cudaMemcpyAsync(c->d_flag, &fb, sizeof fb, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+                g_nccl.AllReduce(c->d_flag, c->d_flag, 1, ncclUint64, ncclMin, c->comm, c->stream) != ncclSuccess ||
+                cudaMemcpyAsync(&fb, c->d_flag, sizeof fb, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                wait_stream(c, c->stream) != LBM_OK)
+                return bail(fail(c, LBM_ENCCL, "agreeing on the storage across ranks failed"));
+            freeb = size_t(fb);
+        }
         const size_t es_ = dt == LBM_F64 ? 8 : 4;
-        const size_t plane_x = size_t(kQ) * ny * size_t(round_up(nz, int(32 / es_))) * es_;
+        lbm_halo_plan tp;
+        fill_plan(nx, ny, nz, es_, o.bc, 0, nslab_total, nxl, 0, &tp);
+        const size_t plane_x = size_t(tp.plane_x) * es_;
         const size_t gap = size_t(dt == LBM_F64 ? k2_sc_gap<double>() : k2_sc_gap<float>());
         const size_t two = size_t(sw) * 2 * (size_t(nxl) + 4) * plane_x;
         const size_t lattice = (size_t(nxl) + 4) * plane_x;
@@ -1273,7 +1458,6 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
             if (cudaMemset(s.buf[b], 0, bytes) != cudaSuccess) return bail(fail(c, LBM_ECUDA, "cudaMemset"));
         }
     }
-    if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess) return bail(fail(c, LBM_ENOMEM, "cudaMalloc flag"));
     if (c->sc && cudaMalloc(&c->sc_sync, sizeof(unsigned) * (size_t(nxl) + 1)) != cudaSuccess)
         return bail(fail(c, LBM_ENOMEM, "cudaMalloc ring tickets"));
     if (o.kernel == LBM_KERNEL_AA || c->sc) {
@@ -1291,44 +1475,6 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
             return bail(fail(c, LBM_ENOMEM, "cudaMalloc staging (%zu bytes)", c->stage_bytes));
         }
     }
-    if (o.stream) {
-        c->stream = static_cast<cudaStream_t>(o.stream);
-    } else {
-        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
-            return bail(fail(c, LBM_ECUDA, "cudaStreamCreate"));
-        c->own_stream = true;
-    }
-    {
-        int lo = 0, hi = 0;
-        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
-            cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
-            cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming) != cudaSuccess)
-            return bail(fail(c, LBM_ECUDA, "comm stream / events"));
-        // Overlap the exchange with the interior sweep where the exchange
-        // crosses NVLink (NCCL).  On one device (LOCAL slabs, the periodic
-        // wrap) the copies are cheaper than the extra edge launches the split
-        // costs (measured 8 LOCAL slabs: 31.7k MLUPS serial vs 29.9k split),
-        // so there it is off.  LBM_OVERLAP=0/1 forces it (A/B runs, tests).
-        const char* e = getenv("LBM_OVERLAP");
-        c->overlap = e ? e[0] == '1' : o.comm == LBM_COMM_NCCL;
-        const char* f = getenv("LBM_FUSED_HALO");
-        c->fused_halo = !(f && f[0] == '0');
-        if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
-            return bail(fail(c, LBM_ECUDA, "copy stream"));
-        c->chunk_events.resize(9);  // 8 x chunks + the copy stream's completion
-        for (cudaEvent_t& ev : c->chunk_events)
-            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
-                return bail(fail(c, LBM_ECUDA, "read-back events"));
-    }
-    if (o.comm == LBM_COMM_NCCL) {
-        if (!nccl_load()) return bail(fail(c, LBM_ENCCL, "cannot load libnccl.so.2"));
-        ncclUniqueId id;
-        memcpy(&id, o.nccl_id, sizeof id);
-        ncclResult_t r = g_nccl.CommInitRank(&c->comm, o.world, id, o.rank);
-        if (r != ncclSuccess)
-            return bail(fail(c, LBM_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
-    }
     if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(c, LBM_ECUDA, "create sync"));
     *out = c;
     return LBM_OK;
@@ -1336,9 +1482,14 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
 
 void lbm_destroy(lbm_ctx* c) {
     if (!c) return;
+    DeviceGuard dg;
     cudaSetDevice(c->device);
-    if (c->stream) cudaStreamSynchronize(c->stream);
+    // a failed wait (lost peer) aborts the communicator itself
+    if (c->stream && !c->poisoned) wait_stream(c, c->stream);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+    else if (c->comm && g_nccl.CommAbort) g_nccl.CommAbort(c->comm);
+    for (cudaEvent_t ev : c->progress)
+        if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->events) {
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
@@ -1366,18 +1517,21 @@ void lbm_destroy(lbm_ctx* c) {
 }
 
 lbm_status lbm_init_equilibrium(lbm_ctx* c, const double* rho, const double* u) {
+    DeviceGuard dg;
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
     return c->dt == LBM_F64 ? init_eq<double>(c, rho, u, true) : init_eq<float>(c, rho, u, true);
 }
 
 lbm_status lbm_init_equilibrium_device(lbm_ctx* c, const double* rho, const double* u) {
+    DeviceGuard dg;
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
     return c->dt == LBM_F64 ? init_eq<double>(c, rho, u, false) : init_eq<float>(c, rho, u, false);
 }
 
 lbm_status lbm_set_populations(lbm_ctx* c, const double* f) {
+    DeviceGuard dg;
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
     if (!f) return fail(c, LBM_EINVAL, "f is NULL");
@@ -1385,6 +1539,7 @@ lbm_status lbm_set_populations(lbm_ctx* c, const double* f) {
 }
 
 lbm_status lbm_step(lbm_ctx* c, long n) {
+    DeviceGuard dg;
     if (c && n < 0) return fail(c, LBM_EINVAL, "n must be >= 0 (got %ld)", n);
     lbm_status st = entry(c, true);
     if (st != LBM_OK) return st;
@@ -1392,25 +1547,28 @@ lbm_status lbm_step(lbm_ctx* c, long n) {
 }
 
 lbm_status lbm_macroscopic(lbm_ctx* c, double* rho, double* u) {
+    DeviceGuard dg;
     lbm_status st = entry(c, true);
     if (st != LBM_OK) return st;
     return c->dt == LBM_F64 ? macro<double>(c, rho, u, true) : macro<float>(c, rho, u, true);
 }
 
 lbm_status lbm_macroscopic_device(lbm_ctx* c, double* rho, double* u) {
+    DeviceGuard dg;
     lbm_status st = entry(c, true);
     if (st != LBM_OK) return st;
     return c->dt == LBM_F64 ? macro<double>(c, rho, u, false) : macro<float>(c, rho, u, false);
 }
 
 lbm_status lbm_get_populations_box(lbm_ctx* c, int x0, int y0, int z0, int lx, int ly, int lz, double* f) {
+    DeviceGuard dg;
     lbm_status st = entry(c, true);
     if (st != LBM_OK) return st;
     if (!f) return fail(c, LBM_EINVAL, "f is NULL");
     if (lx < 0 || ly < 0 || lz < 0 || x0 < 0 || y0 < 0 || z0 < 0 || x0 + lx > c->nxl_proc || y0 + ly > c->ny ||
         z0 + lz > c->nz)
         return fail(c, LBM_EINVAL, "box outside the slab");
-    if ((long long)lx * ly * lz == 0) return LBM_OK;
+    if ((long long)lx * ly * lz == 0) return ensure_ghosts(c);  // collective under NCCL: every rank exchanges
     return c->dt == LBM_F64 ? get_box<double>(c, x0, y0, z0, lx, ly, lz, f)
                             : get_box<float>(c, x0, y0, z0, lx, ly, lz, f);
 }
@@ -1421,10 +1579,10 @@ lbm_status lbm_get_populations(lbm_ctx* c, double* f) {
 }
 
 lbm_status lbm_synchronize(lbm_ctx* c) {
+    DeviceGuard dg;
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
-    CK(cudaStreamSynchronize(c->stream));
-    return LBM_OK;
+    return wait_stream(c, c->stream);
 }
 
 lbm_status lbm_get_time(const lbm_ctx* c, long* t) {
@@ -1445,6 +1603,7 @@ lbm_status lbm_nccl_unique_id(void* out128) {
 }
 
 lbm_status lbm_profile_enable(lbm_ctx* c, int on) {
+    DeviceGuard dg;
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
     c->profiling = on != 0;
@@ -1452,18 +1611,20 @@ lbm_status lbm_profile_enable(lbm_ctx* c, int on) {
 }
 
 lbm_status lbm_profile_reset(lbm_ctx* c) {
+    DeviceGuard dg;
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
-    CK(cudaStreamSynchronize(c->stream));
+    if ((st = wait_stream(c, c->stream)) != LBM_OK) return st;
     c->events_used = 0;
     return LBM_OK;
 }
 
 lbm_status lbm_get_stats(lbm_ctx* c, lbm_stats* s) {
+    DeviceGuard dg;
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
     if (!s) return fail(c, LBM_EINVAL, "stats is NULL");
-    CK(cudaStreamSynchronize(c->stream));
+    if ((st = wait_stream(c, c->stream)) != LBM_OK) return st;
     memset(s, 0, sizeof *s);
     s->launches = c->launches;
     s->k1_launches = c->k1_launches;

@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "kernels.h"
@@ -159,12 +160,27 @@ __device__ __forceinline__ int wrapi(int v, int n) {
     return w;
 }
 
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 }  // namespace
+
+// EXPERIMENT flags (temporary, LBM_EXP env): bit 0 = periodic: skip wrapped
+// sources (wrong results, timing only); bit 1 = TMA loads evict_last;
+// bit 2 = TMA loads evict_first
+__device__ int g_k2_exp = 0;
 
 template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
 __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     k2_sweep(const __grid_constant__ CUtensorMap tmA, const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
-             int xbeg, int xend, int chunk, int out_poff, unsigned* __restrict__ sc_sync, T* haloL, T* haloR) {
+             int xbeg, int xend, int chunk, int out_poff, unsigned* __restrict__ sc_sync, T* haloL, T* haloR,
+             int xbeg2, int nch1) {
     using C = K2Cfg<T, TY, TZ>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* const stage = reinterpret_cast<T*>(smem_raw);
@@ -216,8 +232,11 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const int ntz = (g.nz + TZ - 1) / TZ;
     const int y0 = (item_t / ntz) * TY;
     const int z0 = (item_t % ntz) * TZ;
-    const int xs = xbeg + item_c * chunk;
-    const int xe = min(xs + chunk, xend);
+    // chunks [0, nch1) cover [xbeg, xend); chunks nch1.. the second range
+    // [xbeg2, xbeg2 + xend - xbeg) (the two edge ranges of an overlapped sweep)
+    const bool r2 = item_c >= nch1;
+    const int xs = r2 ? xbeg2 + (item_c - nch1) * chunk : xbeg + item_c * chunk;
+    const int xe = min(xs + chunk, r2 ? xbeg2 + (xend - xbeg) : xend);
     if (xs >= xe) {
         sc_finish(xs);
         return;
@@ -253,14 +272,22 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool edge_y = (y0 < 2) || (y0 + TY + 2 > g.ny);
     const bool edge_z = (z0 < 2) || (z0 + TZ + 2 > g.nz);
 
+    const int exp = g_k2_exp;
+    uint64_t pol = 0;
+    if (exp & 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    if (exp & 4) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     auto issue = [&](int p, int s) {  // one thread: stage plane p into buffer s
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_expect_tx(&bar[s], C::TX_BYTES);
         static_for<0, kQ>([&](auto kc) {
             constexpr int k = decltype(kc)::value;
             constexpr int i = slot_dir(k);
-            tma_load_3d(stage + (s * kQ + k) * C::BOXE, &tmA, &bar[s], z0 - C::ZPAD, y0 - 1 - can_cy(i),
-                        plane_slot_t<RING>(g, p - can_cx(i)) * kQ + k);
+            if (exp & 6)
+                tma_load_3d_hint(stage + (s * kQ + k) * C::BOXE, &tmA, &bar[s], z0 - C::ZPAD, y0 - 1 - can_cy(i),
+                                 plane_slot_t<RING>(g, p - can_cx(i)) * kQ + k, pol);
+            else
+                tma_load_3d(stage + (s * kQ + k) * C::BOXE, &tmA, &bar[s], z0 - C::ZPAD, y0 - 1 - can_cy(i),
+                            plane_slot_t<RING>(g, p - can_cx(i)) * kQ + k);
         });
     };
 
@@ -335,7 +362,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool zlo = z0 == 0, zhi = z0 + TZ >= g.nz;
     const bool zpre = kZPre && zlo != zhi && g.nz % TZ == 0;
     const int zs = zlo ? 1 : -1;  // c_z of the slots that wrap on side 1
-    const int zside = !zpre || !act1 ? -1
+    const int zside = !zpre || !act1 || (exp & 1) ? -1
                       : zlo ? (b == 0 ? 0 : (b == 1 ? 1 : -1)) : (b == TZ + 1 ? 0 : (b == TZ ? 1 : -1));
     auto zwrap_prefetch = [&](int pn, int buf) {
         if constexpr (kZPre) {
@@ -385,7 +412,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         // used an integer division).  With zpre the z-wrap lanes take theirs
         // from the prefetch instead.
         T fs[kQ];
-        const bool wdir = BC == BC_PERIODIC && has1 && (edge_y || (edge_z && !zpre)) && act1;
+        const bool wdir = BC == BC_PERIODIC && has1 && (edge_y || (edge_z && !zpre)) && act1 && !(exp & 1);
         auto wraps = [&](int cy, int cz) {
             const int sy = qy - cy, sz = qz - cz;
             const bool zw = sz < 0 || sz >= g.nz;
@@ -679,13 +706,27 @@ int tile_choice(int esize) {
     return c;
 }
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    return dev;
+}
+
 int num_sms() {
-    static int n = 0;
+    static std::atomic<int> cache[kMaxDevices];  // 0 = not yet queried (per device ordinal)
+    const int dev = current_device();
+    int n = cache[dev].load(std::memory_order_relaxed);
     if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 148;
+        }
+        cache[dev].store(n, std::memory_order_relaxed);
     }
     return n;
 }
@@ -700,18 +741,30 @@ constexpr int k2_max_chunk(bool wide = false) {
 
 template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
 cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, int out_poff,
-                           unsigned* sc_sync, T* haloL, T* haloR, cudaStream_t s) {
+                           unsigned* sc_sync, T* haloL, T* haloR, cudaStream_t s, int xbeg2 = 0, int nxs2 = 0) {
     using C = K2Cfg<T, TY, TZ>;
     constexpr int NT = C::NT;
     auto kern = k2_sweep<T, BC, TY, TZ, EARLY, RING>;
-    static int occ = -1;
-    if (occ < 0) {
+    // The large-shared-memory opt-in is a per-device (per-context) function
+    // attribute: set it once per device ordinal this process launches on
+    // (setting it twice from racing threads is harmless).
+    static std::atomic<int> occ_cache[kMaxDevices];  // 0 = not yet set on that device
+    const int dev = current_device();
+    int occ = occ_cache[dev].load(std::memory_order_acquire);
+    if (occ < 1) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
         if (e != cudaSuccess) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, C::SMEM);
         if (e != cudaSuccess) return e;
         if (occ < 1) return cudaErrorInvalidConfiguration;
+        occ_cache[dev].store(occ, std::memory_order_release);
     }
+    static const bool exp_set = [] {
+        const char* e = getenv("LBM_EXP");
+        const int v = e ? atoi(e) : 0;
+        return cudaMemcpyToSymbol(g_k2_exp, &v, sizeof v) == cudaSuccess;
+    }();
+    if (!exp_set) return cudaErrorUnknown;
     EncodeFn enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     const SlabGeom& g = P.g;
@@ -757,10 +810,11 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     const int kMaxChunk = wide ? k2_max_chunk<T>(true) : k2_max_chunk<T>(false);
     int best = 1;
     double best_cost = 1e300;
+    const int ranges = nxs2 > 0 ? 2 : 1;
     for (int nch = 1; nch <= nxs; ++nch) {
         const int chunk = (nxs + nch - 1) / nch;
         if (chunk > kMaxChunk && nch < nxs) continue;
-        const long long items = ntiles * ((nxs + chunk - 1) / chunk);
+        const long long items = ntiles * ((nxs + chunk - 1) / chunk) * ranges;
         const double waves = double((items + slots - 1) / slots);
         const double cost = waves * (chunk + 2.5);
         if (cost < best_cost - 1e-9) {
@@ -776,12 +830,14 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     }();
     if (force_chunk > 0) chunk = min(force_chunk, nxs);
     if (sc_sync) chunk = min(chunk, kMaxChunk);  // the ring gap assumes it (k2_sc_gap)
-    const dim3 grid(unsigned(ntiles), unsigned((nxs + chunk - 1) / chunk));
+    const int nch1 = (nxs + chunk - 1) / chunk;
+    const dim3 grid(unsigned(ntiles), unsigned(nch1 * ranges));
     if (sc_sync) {  // tickets and per-chunk completion counters start at zero
         cudaError_t e = cudaMemsetAsync(sc_sync, 0, sizeof(unsigned) * (1 + grid.y), s);
         if (e != cudaSuccess) return e;
     }
-    kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk, out_poff, sc_sync, haloL, haloR);
+    kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk, out_poff, sc_sync, haloL, haloR, xbeg2,
+                                   nch1);
     return cudaGetLastError();
 }
 
@@ -808,7 +864,8 @@ int k2_sc_gap() {
 
 template <typename T>
 cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s, int out_poff,
-                      unsigned* sc_sync, T* halo_left, T* halo_right) {
+                      unsigned* sc_sync, T* halo_left, T* halo_right, int xbeg2, int nxs2) {
+    if (nxs2 > 0 && (nxs2 != nxs || sc_sync)) return cudaErrorInvalidValue;
     if (nxs <= 0) return cudaSuccess;
     const bool per = P.g.bc == BC_PERIODIC;
     // Default: read the stage into registers and issue the next TMA before
@@ -828,10 +885,10 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
 #define LBM_K2_TILE_CASE(TY, TZ)                                                                              \
     if constexpr (K2Cfg<T, TY, TZ>::FITS) {                                                                   \
         if (early)                                                                                            \
-            return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s) \
-                       : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s);  \
-        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s)    \
-                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s);     \
+            return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s, xbeg2, nxs2) \
+                       : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s, xbeg2, nxs2);  \
+        return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s, xbeg2, nxs2)    \
+                   : launch_k2_impl<T, BC_CAVITY, TY, TZ, false, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s, xbeg2, nxs2);     \
     } else {                                                                                                  \
         return cudaErrorInvalidConfiguration;                                                                 \
     }
@@ -853,9 +910,9 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
 template bool k2_supported<double>(const SlabGeom&);
 template bool k2_supported<float>(const SlabGeom&);
 template cudaError_t launch_k2<double>(const double*, double*, const StepParams<double>&, int, int, cudaStream_t,
-                                       int, unsigned*, double*, double*);
+                                       int, unsigned*, double*, double*, int, int);
 template cudaError_t launch_k2<float>(const float*, float*, const StepParams<float>&, int, int, cudaStream_t, int,
-                                      unsigned*, float*, float*);
+                                      unsigned*, float*, float*, int, int);
 template int k2_sc_gap<double>();
 template int k2_sc_gap<float>();
 

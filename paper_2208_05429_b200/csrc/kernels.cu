@@ -15,12 +15,14 @@ namespace lbm {
 // One thread per cell; a warp covers 32 consecutive z of one row, so each of
 // the 19 loads and 19 stores of a warp is one contiguous 256 B (fp64) or
 // 128 B (fp32) segment (shifted by one element for c_z != 0 directions).
+// Planes [xbeg, xbeg + n1) and then [xbeg2, ...): the two edge ranges of an
+// overlapped X-slab sweep run as one grid (api.cu run_steps).
 template <typename T, int BC>
 __global__ void __launch_bounds__(256) k1_step(const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
-                                              int xbeg) {
+                                              int xbeg, int n1, int xbeg2) {
     const int z = blockIdx.x * 32 + threadIdx.x;
     const int y = blockIdx.y * 8 + threadIdx.y;
-    const int x = xbeg + blockIdx.z;
+    const int x = int(blockIdx.z) < n1 ? xbeg + int(blockIdx.z) : xbeg2 + (int(blockIdx.z) - n1);
     if (z >= P.g.nz || y >= P.g.ny) return;
     T f[kQ];
     pull_cell<T, BC>(A, P, x, y, z, f);
@@ -359,12 +361,15 @@ static dim3 cell_grid(int nz, int ny, int nxs) { return dim3((nz + 31) / 32, (ny
 static const dim3 kBlock(32, 8, 1);
 
 template <typename T>
-cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s) {
-    if (nxs <= 0) return cudaSuccess;
+cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s, int xbeg2,
+                      int nxs2) {
+    if (nxs < 0 || nxs2 < 0) return cudaErrorInvalidValue;
+    if (nxs + nxs2 == 0) return cudaSuccess;
+    const dim3 grid = cell_grid(P.g.nz, P.g.ny, nxs + nxs2);
     if (P.g.bc == BC_PERIODIC)
-        k1_step<T, BC_PERIODIC><<<cell_grid(P.g.nz, P.g.ny, nxs), kBlock, 0, s>>>(A, B, P, xbeg);
+        k1_step<T, BC_PERIODIC><<<grid, kBlock, 0, s>>>(A, B, P, xbeg, nxs, xbeg2);
     else
-        k1_step<T, BC_CAVITY><<<cell_grid(P.g.nz, P.g.ny, nxs), kBlock, 0, s>>>(A, B, P, xbeg);
+        k1_step<T, BC_CAVITY><<<grid, kBlock, 0, s>>>(A, B, P, xbeg, nxs, xbeg2);
     return cudaGetLastError();
 }
 
@@ -456,7 +461,7 @@ cudaError_t launch_k3_moments(const T* A, const StepParams<T>& P, int xbeg, int 
 }
 
 #define LBM_INSTANTIATE(T)                                                                                   \
-    template cudaError_t launch_k1<T>(const T*, T*, const StepParams<T>&, int, int, cudaStream_t);           \
+    template cudaError_t launch_k1<T>(const T*, T*, const StepParams<T>&, int, int, cudaStream_t, int, int);           \
     template cudaError_t launch_k1_sc<T>(T*, const StepParams<T>&, int, unsigned*, cudaStream_t, bool);      \
     template cudaError_t launch_k0_equilibrium<T>(const double*, const double*, T*, const SlabGeom&,         \
                                                   cudaStream_t, int, int);                                   \

@@ -6,9 +6,11 @@
 namespace lbm {
 
 // K1: one fused collide+stream step, A = f*(t-1) -> B = f*(t), slab-local
-// planes [xbeg, xbeg + nxs).  A's ghost planes must be valid.
+// planes [xbeg, xbeg + nxs) and [xbeg2, xbeg2 + nxs2) (one grid: the two
+// edge ranges of an overlapped sweep).  A's ghost planes must be valid.
 template <typename T>
-cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s);
+cudaError_t launch_k1(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s, int xbeg2 = 0,
+                      int nxs2 = 0);
 
 // K1 in place on single-copy ring storage: output plane x to ring slot
 // x + 2 + out_poff (= the slot of input plane x - 4); sync = device scratch
@@ -28,19 +30,17 @@ constexpr int kK1ScGap = 4;
 // Fused halo (two-buffer storage only): halo_left / halo_right = the next-sweep
 // buffer of the left / right neighbour slab (or this slab's own, periodic
 // single slab), which then receives its ghost planes from this sweep's stores.
+// Two ranges (xbeg2, nxs2 > 0; two-buffer storage only): planes [xbeg2,
+// xbeg2 + nxs2) in the same grid, nxs2 == nxs (the edge ranges of an
+// overlapped X-slab sweep: one launch instead of two).
 template <typename T>
 cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s, int out_poff = 0,
-                      unsigned* sc_sync = nullptr, T* halo_left = nullptr, T* halo_right = nullptr);
+                      unsigned* sc_sync = nullptr, T* halo_left = nullptr, T* halo_right = nullptr, int xbeg2 = 0,
+                      int nxs2 = 0);
 template <typename T>
 int k2_sc_gap();
 template <typename T>
 bool k2_supported(const SlabGeom& g);
-// K2R: the same two-step sweep with register-staged gathers and two warp
-// groups (k2r.cu); any geometry.
-template <typename T>
-bool k2r_supported(const SlabGeom& g);
-template <typename T>
-cudaError_t launch_k2r(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, cudaStream_t s);
 
 // canonical feq of planes [xbeg, xbeg + nxc) (nxc < 0: the whole slab); rho/u
 // point at the first of those planes

@@ -77,6 +77,9 @@ def test_create_rejects_bad_kernel_choices():
     o.kernel = -1
     with pytest.raises(lbm.LbmError, match="bad kernel"):
         lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+    o.kernel = lbm.LBM_KERNEL_K2_REG  # reserved: the removed cp.async variant
+    with pytest.raises(lbm.LbmError, match="removed"):
+        lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
 
 
 def test_header_enums_match_binding():

@@ -194,15 +194,15 @@ K2_DIMS = [(1, 8, 32), (2, 5, 7), (3, 9, 33), (7, 8, 32), (16, 16, 64), (5, 17, 
 @pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_k2_equals_k1_bitwise(dims, bc, dtype):
-    """The two-step sweeps -- K2 (TMA-staged) and K2_REG (cp.async-staged,
-    warp-specialised) -- reproduce two one-step sweeps (K1) bit for bit: ragged
+    """The two-step sweep K2 (TMA-staged) and its single-copy ring form
+    K2_SC reproduce two one-step sweeps (K1) bit for bit: ragged
     tiles, tiles touching every wall, x-chunk seams, thin slabs, both BCs,
     both dtypes; and all match the oracle."""
     if bc == lbm.LBM_BC_PERIODIC and dims[0] < 2:
         pytest.skip("periodic needs >= 2 planes")
     f0 = li.random_populations(31, *dims)
     res = {}
-    for kernel in (lbm.LBM_KERNEL_K1, lbm.LBM_KERNEL_K2, lbm.LBM_KERNEL_K2_REG):
+    for kernel in (lbm.LBM_KERNEL_K1, lbm.LBM_KERNEL_K2, lbm.LBM_KERNEL_K2_SC):
         with lbm.Lattice(*dims, 0.6, LID, dtype, bc=bc, kernel=kernel) as lat:
             lat.set_populations(f0)
             lat.step(4)
@@ -211,12 +211,11 @@ def test_k2_equals_k1_bitwise(dims, bc, dtype):
             if kernel != lbm.LBM_KERNEL_K1:
                 assert st.k2_launches == 2 and st.k1_launches == 0
     assert np.array_equal(res[lbm.LBM_KERNEL_K1], res[lbm.LBM_KERNEL_K2])
-    assert np.array_equal(res[lbm.LBM_KERNEL_K1], res[lbm.LBM_KERNEL_K2_REG])
+    assert np.array_equal(res[lbm.LBM_KERNEL_K1], res[lbm.LBM_KERNEL_K2_SC])
     assert relerr_floor(res[lbm.LBM_KERNEL_K2], oracle.run(f0, bc, 0.6, LID, 4)) <= TOL[dtype]
 
 
-K2_VARIANTS = [("LBM_K2R_CFG", v, 3) for v in ["8x32s0", "8x32s1", "8x16s0m2", "16x16s0", "4x32s0m2", "8x16s1m2"]] + \
-    [("LBM_K2_TILE", v, 2) for v in ["8x32", "8x16", "16x16"]] + [("LBM_K2_EARLY", "0", 2), ("LBM_K2_CHUNK", "3", 2)]
+K2_VARIANTS = [("LBM_K2_TILE", v, 2) for v in ["8x32", "8x16", "16x16"]] + [("LBM_K2_EARLY", "0", 2), ("LBM_K2_CHUNK", "3", 2)]
 
 
 @pytest.mark.parametrize("fused", ["0", "1"])
@@ -287,7 +286,7 @@ def test_k2_local_slabs_bitwise(bc):
     f0 = li.random_populations(32, *dims)
     outs = []
     for kernel, slabs in [(lbm.LBM_KERNEL_K1, 1), (lbm.LBM_KERNEL_K2, 1), (lbm.LBM_KERNEL_K2, 2),
-                          (lbm.LBM_KERNEL_K2, 8), (lbm.LBM_KERNEL_K2_REG, 2)]:
+                          (lbm.LBM_KERNEL_K2, 8), (lbm.LBM_KERNEL_K2_SC, 2)]:
         comm = lbm.LBM_COMM_LOCAL if slabs > 1 else lbm.LBM_COMM_NONE
         with lbm.Lattice(*dims, 0.55, LID, "f64", bc=bc, kernel=kernel, comm=comm, local_slabs=slabs) as lat:
             lat.set_populations(f0)
@@ -470,7 +469,7 @@ def test_full_size_sampled_parity(cfg_id, dtype, kernel):
 
 def test_randomised_configurations_bitwise():
     """Property check over random small lattices (seeded): for any dims,
-    boundary mode, dtype, kernel (K2, K2_REG, AA), slab count and split of
+    boundary mode, dtype, kernel (K2, K2_SC, AA), slab count and split of
     the step count, the result equals K1 on one slab bit for bit (AA: no
     lid, see test_aa_single_copy_equals_k1), and K1 matches the oracle."""
     rng = np.random.default_rng(2208)
@@ -482,7 +481,7 @@ def test_randomised_configurations_bitwise():
         if bc == lbm.LBM_BC_PERIODIC and dims[0] < 2:
             continue
         dtype = str(rng.choice(["f64", "f32"]))
-        kernel = int(rng.choice([lbm.LBM_KERNEL_K2, lbm.LBM_KERNEL_K2_REG, lbm.LBM_KERNEL_AA]))
+        kernel = int(rng.choice([lbm.LBM_KERNEL_K2, lbm.LBM_KERNEL_K2_SC, lbm.LBM_KERNEL_AA]))
         lid = (0.0, 0.0, 0.0) if kernel == lbm.LBM_KERNEL_AA else (float(rng.uniform(-0.05, 0.05)),
                                                                     float(rng.uniform(-0.05, 0.05)), 0.0)
         splits = [int(v) for v in rng.integers(0, 4, size=int(rng.integers(1, 4)))]

@@ -195,6 +195,20 @@ def test_step_equals_brute_force(dims, periodic):
     assert np.max(np.abs(got - ref)) <= 1e-15
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+@pytest.mark.parametrize("periodic", [False, True])
+def test_run_equals_brute_force_steps(n, periodic):
+    """oracle.run (two lattices, collide in place, pull, swap) equals n
+    independent brute-force steps, odd and even n."""
+    f = li.random_populations(4, 4, 5, 6)
+    bc = oracle.BC_PERIODIC if periodic else oracle.BC_CAVITY
+    ref = f
+    for _ in range(n):
+        ref = brute_force_step(ref, 0.6, LID, periodic)
+    got = oracle.run(f, bc, 0.6, LID, n)
+    assert np.max(np.abs(got - ref)) <= 1e-14 * n
+
+
 @pytest.mark.parametrize("dims", [(3, 3, 3), (4, 4, 4), (5, 6, 7), (6, 4, 5)])
 def test_step_equals_fuse_swap_alg1_bitwise(dims):
     """Alg. 1: Stage I collide+revert on the faces,

@@ -19,8 +19,10 @@ run 's/v = v + 6.0 \* W\[i\]/v = v - 6.0 * W[i]/' "lid term sign"
 run 's/if (sz >= nz) {/if (sz < 0) {/' "lid on the wrong z face"
 run 's/int sx = gx - C\[i\]\[0\]/int sx = gx + C[i][0]/' "push instead of pull in x"
 run 's/v = fstar\[idx(OPP\[i\], x, y, z/v = fstar[idx(i, x, y, z/' "bounce-back without opp"
-run 's/const double omega = 1.0 \/ tau;/const double omega = 1.0 \/ (tau + 0.0001);/' "tau convention"
+run 's/1.0 \/ tau,/1.0 \/ (tau + 0.0001),/' "tau convention"
 run 's/{-1, 0, -1}, {-1, 0, 1}/{-1, 0, 1}, {-1, 0, -1}/' "directions 6,7 transposed"
 run 's/feq\[0\] = rest;/feq[0] = W[0] * rho * (1.0 - 1.5 * usq);/' "no rest-population closure"
 run 's/u\[a\] = j\[a\] \/ r;/u[a] = j[a] \/ (r + 1e-9);/' "perturbed velocity division"
+run 's/a = b;$/a = a;/' "run: lattices not swapped"
+run 's/if (a != f) memcpy/if (0) memcpy/' "run: odd-step result not copied back"
 rm -rf "$SCR"

@@ -3,7 +3,7 @@ the library's two-step (or one-step) sweep launches with the library's own
 CUDA events on a cavity/periodic box and prints one line per run.
 
   python tools/sweep_bench.py --dims 256,512,512 --dtype f64 --kernel k2 --steps 40 --reps 3
-Variant shapes are selected by the env vars LBM_K2R_CFG / LBM_K2_TILE."""
+Variant shapes are selected by the env vars LBM_K2_TILE."""
 import argparse
 import os
 import statistics
@@ -28,7 +28,7 @@ ap.add_argument("--slabs", type=int, default=1, help="LOCAL X-slabs on this GPU 
 ap.add_argument("--power", action="store_true", help="also sample SM clock and board power (NVML)")
 a = ap.parse_args()
 nx, ny, nz = (int(v) for v in a.dims.split(","))
-kern = {"auto": 0, "k1": 1, "k2": 2, "k2reg": 3, "aa": 4, "k2sc": 5}[a.kernel]
+kern = {"auto": 0, "k1": 1, "k2": 2, "aa": 4, "k2sc": 5}[a.kernel]
 bc = lbm.LBM_BC_CAVITY if a.bc == "cavity" else lbm.LBM_BC_PERIODIC
 es = 8 if a.dtype == "f64" else 4
 kw = dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=a.slabs) if a.slabs > 1 else {}
