@@ -73,7 +73,7 @@
 extern "C" {
 #endif
 
-#define LBM_ABI_VERSION 1
+#define LBM_ABI_VERSION 2
 
 typedef struct lbm_ctx lbm_ctx; /* opaque; library-owned */
 
@@ -148,6 +148,26 @@ typedef enum {
  *         multi-GPU data path emulated on one GPU, for tests) */
 typedef enum { LBM_COMM_NONE = 0, LBM_COMM_NCCL = 1, LBM_COMM_LOCAL = 2 } lbm_comm;
 
+/* How NCCL ranks get their ghost planes.
+ *  AUTO / EXCHANGE  grouped ncclSend/ncclRecv of the 24-slot spans before a
+ *                   sweep, overlapped with the interior sweep.
+ *  PEER             fused cross-GPU halo: the lattice buffers are CUDA VMM
+ *                   allocations mapped into the neighbouring ranks (POSIX
+ *                   descriptors passed over a Unix domain socket, so all
+ *                   ranks must share one host), and every two-step sweep
+ *                   stores the planes its neighbours read straight into
+ *                   their next-sweep buffers over NVLink; consecutive sweeps
+ *                   of neighbours are ordered by stream memory operations
+ *                   (a done-counter per neighbour), the paper's "synchronize
+ *                   at the intersection layers every two time steps"
+ *                   (PAPER.md:747-749).  Needs comm == NCCL (world 1 maps the
+ *                   slab onto itself: the periodic self-wrap), kernel AUTO or
+ *                   K2 (two-buffer storage); EINVAL otherwise, ENCCL if the
+ *                   rendezvous fails.  One-step sweeps (odd remainders) and
+ *                   init still exchange through NCCL.  Bitwise identical to
+ *                   EXCHANGE. */
+typedef enum { LBM_HALO_AUTO = 0, LBM_HALO_EXCHANGE = 1, LBM_HALO_PEER = 2 } lbm_halo;
+
 typedef struct {
     int struct_size;     /* sizeof(lbm_opts), for forward compatibility */
     int bc;              /* lbm_bc */
@@ -158,10 +178,11 @@ typedef struct {
     void *stream;        /* cudaStream_t to run on, or NULL: the context creates one */
     int kernel;          /* lbm_kernel */
     int local_slabs;     /* comm == LOCAL: number of slabs emulated on this device */
+    int halo;            /* lbm_halo (ABI 2) */
 } lbm_opts;
 
 /* Fills *opts with defaults: CAVITY, device -1, rank 0, world 1, NONE,
- * no id, own stream, AUTO, 1 local slab. */
+ * no id, own stream, AUTO, 1 local slab, halo AUTO. */
 void lbm_default_opts(lbm_opts *opts);
 
 /* Create a lattice of nx*ny*nz cells with BGK relaxation time tau
@@ -234,13 +255,20 @@ lbm_status lbm_nccl_unique_id(void *out128);
 typedef struct {
     int nx_local, x0;
     int nz_pitch;            /* z row pitch in elements */
-    long long plane_q;       /* elements per (x, direction) plane = ny * nz_pitch */
+    long long plane_q;       /* elements per (x, direction) plane = (ny + 2 y_ghost) * nz_pitch */
     long long plane_x;       /* elements per x plane = 19 * plane_q */
     long long buffer_elems;  /* (nx_local + 4) * plane_x */
     int left, right;         /* neighbour ranks or -1 */
     long long send_left_off, send_right_off, recv_left_off, recv_right_off;
     long long span;          /* elements per message (24 * plane_q) */
     int dir_of_slot[19];     /* canonical direction stored at internal slot k */
+    /* Periodic boxes: every (x, direction) plane has a ghost frame of
+     * y_ghost (2) rows above and below the ny rows and z_offset elements
+     * (32 bytes) before z = 0 (>= 2 after z = nz-1), holding copies of the
+     * periodically wrapped cells; cavity: 0, 0.  Cell (y, z) of a plane is at
+     * cell0 + y * nz_pitch + z, cell0 = y_ghost * nz_pitch + z_offset. */
+    int y_ghost, z_offset;
+    long long cell0;
 } lbm_halo_plan;
 
 lbm_status lbm_plan_halo(int nx, int ny, int nz, lbm_dtype dtype, int bc, int rank,

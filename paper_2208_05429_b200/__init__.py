@@ -29,6 +29,7 @@ LBM_F64, LBM_F32 = 0, 1
 LBM_BC_CAVITY, LBM_BC_PERIODIC = 0, 1
 LBM_KERNEL_AUTO, LBM_KERNEL_K1, LBM_KERNEL_K2, LBM_KERNEL_K2_REG, LBM_KERNEL_AA, LBM_KERNEL_K2_SC = 0, 1, 2, 3, 4, 5
 LBM_COMM_NONE, LBM_COMM_NCCL, LBM_COMM_LOCAL = 0, 1, 2
+LBM_HALO_AUTO, LBM_HALO_EXCHANGE, LBM_HALO_PEER = 0, 1, 2
 LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_ESTATE, LBM_ENUMERIC = 0, 1, 2, 3, 4, 5, 6
 STATUS = {0: "LBM_OK", 1: "LBM_EINVAL", 2: "LBM_ENOMEM", 3: "LBM_ECUDA", 4: "LBM_ENCCL", 5: "LBM_ESTATE",
           6: "LBM_ENUMERIC"}
@@ -45,7 +46,7 @@ class lbm_opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int), ("bc", ctypes.c_int), ("device", ctypes.c_int),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("comm", ctypes.c_int),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("kernel", ctypes.c_int),
-                ("local_slabs", ctypes.c_int)]
+                ("local_slabs", ctypes.c_int), ("halo", ctypes.c_int)]
 
 
 class lbm_halo_plan(ctypes.Structure):
@@ -54,7 +55,8 @@ class lbm_halo_plan(ctypes.Structure):
                 ("buffer_elems", ctypes.c_longlong), ("left", ctypes.c_int), ("right", ctypes.c_int),
                 ("send_left_off", ctypes.c_longlong), ("send_right_off", ctypes.c_longlong),
                 ("recv_left_off", ctypes.c_longlong), ("recv_right_off", ctypes.c_longlong),
-                ("span", ctypes.c_longlong), ("dir_of_slot", ctypes.c_int * 19)]
+                ("span", ctypes.c_longlong), ("dir_of_slot", ctypes.c_int * 19),
+                ("y_ghost", ctypes.c_int), ("z_offset", ctypes.c_int), ("cell0", ctypes.c_longlong)]
 
 
 class lbm_stats(ctypes.Structure):
@@ -253,9 +255,9 @@ class Lattice:
 
     def __init__(self, nx, ny, nz, tau, u_lid=(0.0, 0.0, 0.0), dtype="f64", bc=LBM_BC_CAVITY,
                  kernel=LBM_KERNEL_AUTO, comm=LBM_COMM_NONE, local_slabs=1, rank=0, world=1,
-                 nccl_id: bytes | None = None, stream=None, device=-1):
+                 nccl_id: bytes | None = None, stream=None, device=-1, halo=0):
         o = lbm_default_opts()
-        o.bc, o.kernel, o.comm, o.local_slabs = bc, kernel, comm, local_slabs
+        o.bc, o.kernel, o.comm, o.local_slabs, o.halo = bc, kernel, comm, local_slabs, halo
         o.rank, o.world, o.device = rank, world, device
         self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         o.nccl_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None

@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(256) k_aa_merge(T* __restrict__ dst, const T* 
     const int sy = y - can_cy(i), sz = z - can_cz(i);
     // periodic: every entry has a (wrapped) writer
     if (g.bc == BC_CAVITY && (sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz)) return;
-    const long long o = (long long)m * g.pq + (long long)y * g.nzp + z;
+    // dst / src point at slot-plane starts: cells begin at g.org (the frame)
+    const long long o = (long long)m * g.pq + g.org + (long long)y * g.nzp + z;
     dst[o] = src[o];
 }
 

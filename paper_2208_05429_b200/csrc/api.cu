@@ -28,6 +28,7 @@
 
 #include "../../include/lbm.h"
 #include "kernels.h"
+#include "peer.h"
 
 using namespace lbm;
 
@@ -114,6 +115,9 @@ struct lbm_ctx {
     std::vector<Slab> slabs;
     int cur = 0;
     bool initialized = false, ghosts_valid = false, poisoned = false;
+    // periodic ghost frame (SlabGeom) of the state buffer's own planes is
+    // current: K2 sweeps keep it, every other writer clears it
+    bool frame_valid = false;
     long t = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -143,6 +147,14 @@ struct lbm_ctx {
     std::vector<cudaEvent_t> progress;
     long long progress_issued = 0, progress_done = 0;
     double nccl_timeout_s = 120.0;
+    // fused cross-GPU halo (LBM_HALO_PEER, peer.cu): the lattice buffers are
+    // VMM allocations mapped into the neighbours; pnb[side][0..2] = the
+    // left (0) / right (1) neighbour's buffer 0, buffer 1 and flag page as
+    // mapped here; peer_seq = phases (sweeps, inits) this rank completed
+    bool peer = false, peer_flush = false;
+    peer::Alloc pmine[2], pflags;
+    peer::Alloc pnb[2][3];
+    unsigned peer_seq = 0;
     size_t esize = 8;
     int* d_flag = nullptr;
     // diagnostics
@@ -267,19 +279,59 @@ lbm_status agree_valid(lbm_ctx* c, int bad, const char* why) {
     return LBM_OK;
 }
 
+// ------------------------------------------------- fused peer halo -----
+// Flag page of a rank: the done-counter written by its left neighbour at
+// byte 0, by its right neighbour at byte 64.  After every phase that reads
+// ghost planes and writes a lattice buffer (init, a sweep) a rank bumps its
+// counter into both neighbours' pages (a stream write, ordered after the
+// phase's stores -- including its stores into the neighbours' buffers -- by
+// the write's system-scope fence); before the next phase, and before any
+// read of its ghost planes, it waits on its own page until both neighbours
+// have completed as many phases.  All ranks run the same phase sequence.
+constexpr size_t kFlagFromLeft = 0, kFlagFromRight = 64;
+
+lbm_status peer_wait(lbm_ctx* c) {
+    if (!c->peer || c->peer_seq == 0) return LBM_OK;
+    const Slab& s = c->slabs[0];
+    char* f = static_cast<char*>(c->pflags.va);
+    if (s.left >= 0) CK(peer::stream_wait_geq(c->stream, f + kFlagFromLeft, c->peer_seq, c->peer_flush));
+    if (s.right >= 0) CK(peer::stream_wait_geq(c->stream, f + kFlagFromRight, c->peer_seq, c->peer_flush));
+    return LBM_OK;
+}
+
+lbm_status peer_signal(lbm_ctx* c) {
+    if (!c->peer) return LBM_OK;
+    c->peer_seq++;
+    const Slab& s = c->slabs[0];
+    // this rank is its left neighbour's right neighbour and vice versa
+    if (s.left >= 0)
+        CK(peer::stream_write(c->stream, static_cast<char*>(c->pnb[0][2].va) + kFlagFromRight, c->peer_seq));
+    if (s.right >= 0)
+        CK(peer::stream_write(c->stream, static_cast<char*>(c->pnb[1][2].va) + kFlagFromLeft, c->peer_seq));
+    return LBM_OK;
+}
+
+
 void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world, int nxl, int x0,
                lbm_halo_plan* p) {
     memset(p, 0, sizeof *p);
     p->nx_local = nxl;
     p->x0 = x0;
-    p->nz_pitch = round_up(nz, int(32 / esize));  // rows start on 32 B sectors
-    p->plane_q = (long long)ny * p->nz_pitch;
-    if (const char* e = getenv("LBM_EXP_PAD")) {  // EXPERIMENT (temporary): "<z elems>,<y rows>"
-        int zp = 0, yp = 0;
-        sscanf(e, "%d,%d", &zp, &yp);
-        p->nz_pitch += zp;
-        p->plane_q = (long long)(ny + yp) * p->nz_pitch;
+    // rows start on 32 B sectors.  Periodic: the ghost frame (SlabGeom) --
+    // 2 rows per side, 32 B of columns before z = 0 (so the cells stay
+    // sector aligned) and >= max(2, 16 B) after nz - 1 (K2's TMA box reach)
+    const int sector = int(32 / esize);
+    if (bc == LBM_BC_PERIODIC) {
+        p->y_ghost = 2;
+        p->z_offset = sector;
+        p->nz_pitch = round_up(sector + nz + std::max(2, int(16 / esize)), sector);
+    } else {
+        p->y_ghost = 0;
+        p->z_offset = 0;
+        p->nz_pitch = round_up(nz, sector);
     }
+    p->cell0 = (long long)p->y_ghost * p->nz_pitch + p->z_offset;
+    p->plane_q = (long long)(ny + 2 * p->y_ghost) * p->nz_pitch;
     p->plane_x = (long long)kQ * p->plane_q;
     p->buffer_elems = (long long)(nxl + 4) * p->plane_x;
     if (bc == LBM_BC_PERIODIC) {
@@ -304,6 +356,14 @@ void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world
 
 bool finite_vec(const double* v) {
     return v == nullptr || (std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]));
+}
+
+// Cell origin of lattice buffer b: kernels address cells from here (the
+// periodic ghost frame lies before it, SlabGeom); exchanges move whole
+// slot-planes from the buffer base.
+template <typename T>
+T* origin(const Slab& s, int b) {
+    return static_cast<T*>(s.buf[b]) + s.g.org;
 }
 
 template <typename T>
@@ -508,6 +568,8 @@ bool has_neighbours(const lbm_ctx* c) {
 }
 
 lbm_status ensure_ghosts(lbm_ctx* c) {
+    lbm_status pst = peer_wait(c);  // the neighbours' stores into this rank's ghost planes are complete
+    if (pst != LBM_OK) return pst;
     if (c->aa) {  // odd phase: the gather reads the neighbours' edge slots
         if (c->aa_odd && !c->ghosts_valid && aa_has_halo(c)) {
             lbm_status st = exchange_aa(c, true);
@@ -558,6 +620,21 @@ lbm_status prof_end(lbm_ctx* c, size_t slot, long long updates) {
 }
 
 // --------------------------------------------------------------- engine --
+// Before a K2 sweep of a periodic box: rebuild the ghost frame of the state's
+// own planes if a non-K2 writer left it stale; the x ghost planes then need
+// a fresh exchange (they carry the neighbours' frames).
+template <typename T>
+lbm_status ensure_frame(lbm_ctx* c, int which) {
+    if (c->frame_valid || c->slabs.empty() || c->slabs[0].g.gy == 0) return LBM_OK;
+    for (Slab& s : c->slabs) {
+        CK(launch_frame_fill<T>(origin<T>(s, which), s.g, c->stream));
+        c->launches++;
+    }
+    c->frame_valid = true;
+    c->ghosts_valid = false;
+    return LBM_OK;
+}
+
 // single-copy AA storage: alternate the in-place even / odd steps (aa.cu)
 template <typename T>
 lbm_status run_steps_aa(lbm_ctx* c, long n) {
@@ -572,7 +649,7 @@ lbm_status run_steps_aa(lbm_ctx* c, long n) {
             if (st != LBM_OK) return st;
         }
         for (Slab& s : c->slabs) {
-            cudaError_t e = launch_aa_step<T>(static_cast<T*>(s.buf[0]), make_params<T>(c, s), c->aa_odd, c->stream);
+            cudaError_t e = launch_aa_step<T>(origin<T>(s, 0), make_params<T>(c, s), c->aa_odd, c->stream);
             if (e != cudaSuccess) return fail(c, LBM_ECUDA, "AA step launch failed: %s", cudaGetErrorString(e));
             c->launches++;
             c->k1_launches++;
@@ -598,7 +675,8 @@ template <typename T>
 lbm_status run_steps_sc(lbm_ctx* c, long n) {
     while (n > 0) {
         const int nsteps = n >= 2 ? 2 : 1;
-        lbm_status st = ensure_ghosts(c);
+        lbm_status st = nsteps == 2 ? ensure_frame<T>(c, 0) : LBM_OK;
+        if (st == LBM_OK) st = ensure_ghosts(c);
         if (st != LBM_OK) return st;
         size_t slot = 0;
         st = prof_begin(c, slot);
@@ -606,7 +684,7 @@ lbm_status run_steps_sc(lbm_ctx* c, long n) {
         long long updates = 0;
         // slabs one after another on the stream (the ticket words are reused)
         for (Slab& s : c->slabs) {
-            T* F = static_cast<T*>(s.buf[0]);
+            T* F = origin<T>(s, 0);
             const StepParams<T> P = make_params<T>(c, s);
             const int shift = nsteps == 2 ? c->sc_gap : kK1ScGap;
             const int out_poff = (s.g.poff - shift + s.g.pmod) % s.g.pmod;
@@ -623,6 +701,7 @@ lbm_status run_steps_sc(lbm_ctx* c, long n) {
         if (st == LBM_OK) st = record_progress(c);
         if (st != LBM_OK) return st;
         c->ghosts_valid = false;
+        c->frame_valid = nsteps == 2;
         c->t += nsteps;
         n -= nsteps;
     }
@@ -642,7 +721,7 @@ lbm_status sc_finish_canonical(lbm_ctx* c) {
     for (Slab& s : c->slabs) {
         const StepParams<T> P = make_params<T>(c, s);
         const int out_poff = (s.g.poff - kK1ScGap + s.g.pmod) % s.g.pmod;
-        cudaError_t e = launch_k1_sc<T>(static_cast<T*>(s.buf[0]), P, out_poff, c->sc_sync, c->stream, true);
+        cudaError_t e = launch_k1_sc<T>(origin<T>(s, 0), P, out_poff, c->sc_sync, c->stream, true);
         if (e != cudaSuccess) return fail(c, LBM_ECUDA, "single-copy unstream failed: %s", cudaGetErrorString(e));
         c->launches++;
         s.g.poff = out_poff;
@@ -650,6 +729,7 @@ lbm_status sc_finish_canonical(lbm_ctx* c) {
     c->cur = 0;
     c->ghosts_valid = false;
     c->initialized = true;
+    c->frame_valid = false;
     c->t = 0;
     return LBM_OK;
 }
@@ -670,23 +750,41 @@ lbm_status run_steps(lbm_ctx* c, long n) {
     // themselves when the neighbours' buffers are addressable here (one
     // device: LOCAL slabs, the periodic self-wrap), so after the first sweep
     // no exchange runs.  LBM_FUSED_HALO=0 turns it off (A/B runs, tests).
-    const bool fuse = tma && c->fused_halo && c->opts.comm != LBM_COMM_NCCL;
+    // With NCCL ranks the same stores go into the neighbours' buffers as
+    // mapped here (LBM_HALO_PEER, peer.cu).
+    const bool fuse = tma && c->fused_halo && (c->opts.comm != LBM_COMM_NCCL || c->peer);
     while (n > 0) {
         const int nsteps = (use_k2 && n >= 2) ? 2 : 1;
         const bool fused = fuse && nsteps == 2;
+        // peer halo: the neighbours finished the previous phase (they no
+        // longer read the buffer this sweep writes into, and their stores
+        // into this rank's ghost planes are complete)
+        lbm_status wst = peer_wait(c);
+        if (wst != LBM_OK) return wst;
         // planes [xbeg, xbeg + nxs) (and [xbeg2, xbeg2 + nxs) in the same grid)
         auto launch = [&](Slab& s, int xbeg, int nxs, int xbeg2 = 0, int nxs2 = 0) -> cudaError_t {
             const StepParams<T> P = make_params<T>(c, s);
-            const T* A = static_cast<const T*>(s.buf[c->cur]);
-            T* B = static_cast<T*>(s.buf[c->cur ^ 1]);
-            T* hl = fused && s.left >= 0 ? static_cast<T*>(c->slabs[s.left].buf[c->cur ^ 1]) : nullptr;
-            T* hr = fused && s.right >= 0 ? static_cast<T*>(c->slabs[s.right].buf[c->cur ^ 1]) : nullptr;
+            const T* A = origin<T>(s, c->cur);
+            T* B = origin<T>(s, c->cur ^ 1);
+            T* hl = nullptr;
+            T* hr = nullptr;
+            if (fused && c->peer) {  // the neighbours' next-sweep buffers, mapped here
+                if (s.left >= 0) hl = static_cast<T*>(c->pnb[0][c->cur ^ 1].va) + s.g.org;
+                if (s.right >= 0) hr = static_cast<T*>(c->pnb[1][c->cur ^ 1].va) + s.g.org;
+            } else if (fused) {
+                if (s.left >= 0) hl = origin<T>(c->slabs[s.left], c->cur ^ 1);
+                if (s.right >= 0) hr = origin<T>(c->slabs[s.right], c->cur ^ 1);
+            }
             return nsteps == 1 ? launch_k1<T>(A, B, P, xbeg, nxs, c->stream, xbeg2, nxs2)
                                : launch_k2<T>(A, B, P, xbeg, nxs, c->stream, 0, nullptr, hl, hr, xbeg2, nxs2);
         };
         // Planes [h, nxl-h) read no ghost plane (h = the sweep's step count),
         // so with neighbours the exchange runs on the comm stream while they
         // are swept; the edge planes follow once the ghosts have landed.
+        if (nsteps == 2) {
+            lbm_status fst = ensure_frame<T>(c, c->cur);
+            if (fst != LBM_OK) return fst;
+        }
         const int h = nsteps;
         bool split = !c->ghosts_valid && has_neighbours(c) && c->overlap;
         for (const Slab& s : c->slabs) split = split && s.g.nxl >= 2 * h + 2;
@@ -724,10 +822,12 @@ lbm_status run_steps(lbm_ctx* c, long n) {
         }
         pst = prof_end(c, slot, updates);
         if (pst == LBM_OK) pst = record_progress(c);
+        if (pst == LBM_OK) pst = peer_signal(c);
         if (pst != LBM_OK) return pst;
         (nsteps == 2 ? c->k2_launches : c->k1_launches) += (long long)c->slabs.size();
         c->cur ^= 1;
         c->ghosts_valid = fused;
+        c->frame_valid = nsteps == 2;
         c->t += nsteps;
         n -= nsteps;
     }
@@ -766,6 +866,7 @@ lbm_status finish_init(lbm_ctx* c, int canon) {
         c->aa_odd = false;
         c->ghosts_valid = false;
         c->initialized = true;
+        c->frame_valid = false;
         c->t = 0;
         return LBM_OK;
     }
@@ -776,13 +877,16 @@ lbm_status finish_init(lbm_ctx* c, int canon) {
     }
     for (Slab& s : c->slabs) {
         const StepParams<T> P = make_params<T>(c, s);
-        CK(launch_k0_unstream<T>(static_cast<const T*>(s.buf[canon]), static_cast<T*>(s.buf[canon ^ 1]), P,
+        CK(launch_k0_unstream<T>(origin<T>(s, canon), origin<T>(s, canon ^ 1), P,
                                  c->stream));
         c->launches++;
     }
+    vst = peer_signal(c);
+    if (vst != LBM_OK) return vst;
     c->cur = canon ^ 1;
     c->ghosts_valid = false;
     c->initialized = true;
+    c->frame_valid = false;
     c->t = 0;
     return LBM_OK;
 }
@@ -794,7 +898,7 @@ lbm_status init_eq_aa(lbm_ctx* c, const double* rho, const double* u, bool host)
     const int cap = int(std::max<long long>(1, (long long)(c->stage_bytes / (4 * sizeof(double))) / plane));
     double* stage = static_cast<double*>(c->stage);
     for (Slab& s : c->slabs) {
-        T* F = static_cast<T*>(s.buf[0]);
+        T* F = origin<T>(s, 0);
         const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;  // process-local cell offset
         if (!host) {
             CK(launch_k0_equilibrium<T>(rho ? rho + xoff : nullptr, u ? u + 3 * xoff : nullptr, F, s.g, c->stream));
@@ -863,6 +967,7 @@ lbm_status sc_init_done(lbm_ctx* c) {
     c->cur = 0;
     c->ghosts_valid = false;
     c->initialized = true;
+    c->frame_valid = false;
     c->t = 0;
     return LBM_OK;
 }
@@ -877,7 +982,7 @@ lbm_status init_eq_sc(lbm_ctx* c, const double* rho, const double* u, bool host)
         double* stage = static_cast<double*>(c->stage);
         c->initialized = false;
         for (Slab& s : c->slabs) {
-            T* F = static_cast<T*>(s.buf[0]);
+            T* F = origin<T>(s, 0);
             const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;
             if (!host) {
                 CK(launch_k0_equilibrium<T>(rho ? rho + xoff : nullptr, u ? u + 3 * xoff : nullptr, F, s.g, c->stream));
@@ -912,7 +1017,7 @@ lbm_status init_eq_sc(lbm_ctx* c, const double* rho, const double* u, bool host)
     }
     Slab& s = c->slabs[0];
     const StepParams<T> P = make_params<T>(c, s);
-    T* F = static_cast<T*>(s.buf[0]);
+    T* F = origin<T>(s, 0);
     if (!host) {
         CK(launch_k0_init_pull<T>(rho, u, nullptr, F, P, 0, s.g.nxl, 0, s.g.nxl, c->stream));
         c->launches++;
@@ -969,7 +1074,7 @@ lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
                 lbm_status st = validate_device(c, stage, kQ * ccells, false, &flag);
                 if (st != LBM_OK) return st;
                 if (flag) return agree_valid(c, 1, "populations must be finite");
-                CK(launch_k0_import<T>(stage, static_cast<T*>(s.buf[0]), s.g, xb, nxc, c->stream));
+                CK(launch_k0_import<T>(stage, origin<T>(s, 0), s.g, xb, nxc, c->stream));
                 c->launches++;
             }
         }
@@ -977,7 +1082,7 @@ lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
     }
     Slab& s = c->slabs[0];
     const StepParams<T> P = make_params<T>(c, s);
-    T* F = static_cast<T*>(s.buf[0]);
+    T* F = origin<T>(s, 0);
     const long long plane = (long long)c->ny * c->nz;
     const int cap =
         int(std::max<long long>(1, (long long)(c->stage_bytes / (kQ * sizeof(double))) / plane - 2));
@@ -1000,6 +1105,9 @@ lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
 
 template <typename T>
 lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
+    // peer halo: no neighbour still writes into (or reads) these buffers
+    lbm_status pst = peer_wait(c);
+    if (pst != LBM_OK) return pst;
     // the state is rewritten from here on: invalid until the init completes
     // (a rejected input leaves it undefined, include/lbm.h)
     c->initialized = false;
@@ -1037,16 +1145,17 @@ lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
         if (c->slabs.size() == 1 && c->opts.world == 1) {
             // one slab spanning the domain: the pull-form state in one pass
             // (k0_init_pull), the staging (host inputs) in the other buffer
-            CK(launch_k0_init_pull<T>(dr, du, nullptr, static_cast<T*>(s.buf[canon]), make_params<T>(c, s), 0,
+            CK(launch_k0_init_pull<T>(dr, du, nullptr, origin<T>(s, canon), make_params<T>(c, s), 0,
                                       s.g.nxl, 0, s.g.nxl, c->stream));
             c->launches++;
             c->cur = canon;
             c->ghosts_valid = false;
             c->initialized = true;
+            c->frame_valid = false;
             c->t = 0;
             return LBM_OK;
         }
-        CK(launch_k0_equilibrium<T>(dr, du, static_cast<T*>(s.buf[canon]), s.g, c->stream));
+        CK(launch_k0_equilibrium<T>(dr, du, origin<T>(s, canon), s.g, c->stream));
         c->launches++;
     }
     return finish_init<T>(c, canon);
@@ -1055,6 +1164,8 @@ lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
 template <typename T>
 lbm_status set_pops(lbm_ctx* c, const double* f) {
     if (c->sc) return set_pops_sc<T>(c, f);
+    lbm_status pst = peer_wait(c);  // peer halo: the neighbours are done with these buffers
+    if (pst != LBM_OK) return pst;
     const long long plane = (long long)c->ny * c->nz;
     const long long proc_cells = (long long)c->nxl_proc * plane;
     // import into the non-state buffer, stage in the state buffer (AA: into
@@ -1075,7 +1186,7 @@ lbm_status set_pops(lbm_ctx* c, const double* f) {
             lbm_status st = validate_device(c, stage, kQ * ccells, false, &flag);
             if (st != LBM_OK) return st;
             if (flag) return agree_valid(c, 1, "populations must be finite");
-            CK(launch_k0_import<T>(stage, static_cast<T*>(s.buf[canon]), s.g, xb, nxc, c->stream));
+            CK(launch_k0_import<T>(stage, origin<T>(s, canon), s.g, xb, nxc, c->stream));
             c->launches++;
         }
     }
@@ -1107,7 +1218,7 @@ lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
     double* stage = static_cast<double*>(c->stage);
     for (Slab& s : c->slabs) {
         const StepParams<T> P = make_params<T>(c, s);
-        const T* F = static_cast<const T*>(s.buf[0]);
+        const T* F = origin<T>(s, 0);
         // AA: the phase-aware moments; single-copy ring: K3 on the window
         auto moments = [&](int xb, int nxc, double* r, double* v) {
             return c->sc ? launch_k3_moments<T>(F, P, xb, nxc, r, v, c->stream, flag)
@@ -1147,7 +1258,7 @@ lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
         const StepParams<T> P = make_params<T>(c, s);
         const long long cells = (long long)s.g.nxl * plane;
         const long long xoff = (long long)(s.g.x0 - c->x0_proc) * plane;
-        const T* A = static_cast<const T*>(s.buf[c->cur]);
+        const T* A = origin<T>(s, c->cur);
         if (host) {
             // x chunks: the moments of chunk j+1 run while chunk j crosses PCIe
             // on the copy stream (the staging buffer holds the whole slab)
@@ -1201,10 +1312,10 @@ lbm_status get_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, d
             const int nxc = int(std::min<long long>(cap_planes, b - xb));
             const long long ccells = (long long)nxc * bplane;
             if (c->aa)
-                CK(launch_aa_materialize<T>(static_cast<const T*>(s.buf[0]), P, c->aa_odd, xb - sx0, by, bz, nxc,
+                CK(launch_aa_materialize<T>(origin<T>(s, 0), P, c->aa_odd, xb - sx0, by, bz, nxc,
                                             ly, lz, stage, c->stream));
             else
-                CK(launch_k3_materialize<T>(static_cast<const T*>(s.buf[c->cur]), P, xb - sx0, by, bz, nxc, ly, lz,
+                CK(launch_k3_materialize<T>(origin<T>(s, c->cur), P, xb - sx0, by, bz, nxc, ly, lz,
                                             stage, c->stream));
             c->launches++;
             CK(cudaMemcpy2DAsync(out + (long long)(xb - bx) * bplane, bcells * sizeof(double), stage,
@@ -1213,6 +1324,55 @@ lbm_status get_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, d
         }
     }
     return wait_stream(c, c->stream);
+}
+
+// LBM_HALO_PEER set-up (after the lattice buffers exist): a flag page,
+// then every rank hands its buffers and flag page to its neighbours as file
+// descriptors over the rendezvous socket and maps theirs (peer.cu).
+lbm_status peer_setup(lbm_ctx* c) {
+    std::string why;
+    if (!peer::alloc(c->device, 128, &c->pflags, &why))
+        return fail(c, LBM_ENOMEM, "peer-halo flag page: %s", why.c_str());
+    CK(cudaMemset(c->pflags.va, 0, 128));
+    c->peer_flush = peer::can_flush_remote_writes(c->device);
+    const Slab& s = c->slabs[0];
+    std::vector<int> mine;
+    for (peer::Alloc* m : {&c->pmine[0], &c->pmine[1], &c->pflags}) {
+        const int fd = peer::export_fd(*m, &why);
+        if (fd < 0) {
+            for (int f : mine) close(f);
+            return fail(c, LBM_ENCCL, "peer-halo export: %s", why.c_str());
+        }
+        mine.push_back(fd);
+    }
+    // rendezvous key: the communicator's unique id (the same on every rank)
+    unsigned long long h = 1469598103934665603ULL;
+    const unsigned char* id = static_cast<const unsigned char*>(c->opts.nccl_id);
+    for (int i = 0; i < 128; ++i) h = (h ^ id[i]) * 1099511628211ULL;
+    char key[32];
+    snprintf(key, sizeof key, "%016llx", h);
+    std::vector<int> peers;
+    if (s.left >= 0) peers.push_back(s.left);
+    if (s.right >= 0) peers.push_back(s.right);
+    std::vector<std::vector<int>> theirs;
+    const bool ok = peer::exchange_fds(key, c->opts.rank, peers, mine, &theirs, c->nccl_timeout_s, &why);
+    for (int f : mine) close(f);
+    if (!ok) return fail(c, LBM_ENCCL, "peer-halo rendezvous: %s", why.c_str());
+    size_t j = 0;
+    for (int side = 0; side < 2; ++side) {
+        if ((side == 0 ? s.left : s.right) < 0) continue;
+        const size_t sizes[3] = {c->pmine[0].size, c->pmine[1].size, c->pflags.size};
+        const size_t grans[3] = {c->pmine[0].gran, c->pmine[1].gran, c->pflags.gran};
+        bool mapped = true;
+        for (int m = 0; m < 3; ++m) {
+            if (mapped && !peer::import_fd(c->device, theirs[j][size_t(m)], sizes[m], grans[m], &c->pnb[side][m], &why))
+                mapped = false;
+            close(theirs[j][size_t(m)]);
+        }
+        if (!mapped) return fail(c, LBM_ENCCL, "peer-halo mapping of rank %d: %s", peers[j], why.c_str());
+        ++j;
+    }
+    return LBM_OK;
 }
 
 }  // namespace
@@ -1235,6 +1395,7 @@ void lbm_default_opts(lbm_opts* o) {
     o->stream = nullptr;
     o->kernel = LBM_KERNEL_AUTO;
     o->local_slabs = 1;
+    o->halo = LBM_HALO_AUTO;
 }
 
 const char* lbm_last_error(const lbm_ctx* c) { return c ? c->err.c_str() : t_last_error.c_str(); }
@@ -1290,6 +1451,11 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     if (o.comm == LBM_COMM_LOCAL && o.world != 1) return fail(c, LBM_EINVAL, "comm LOCAL needs world == 1");
     if (o.comm < LBM_COMM_NONE || o.comm > LBM_COMM_LOCAL) return fail(c, LBM_EINVAL, "bad comm %d", o.comm);
     if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K2_SC) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    if (o.halo < LBM_HALO_AUTO || o.halo > LBM_HALO_PEER) return fail(c, LBM_EINVAL, "bad halo %d", o.halo);
+    if (o.halo == LBM_HALO_PEER && o.comm != LBM_COMM_NCCL)
+        return fail(c, LBM_EINVAL, "halo PEER needs comm NCCL (world 1: the periodic self-wrap)");
+    if (o.halo == LBM_HALO_PEER && o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K2)
+        return fail(c, LBM_EINVAL, "halo PEER needs the two-buffer K2 storage (kernel AUTO or K2)");
     if (o.kernel == LBM_KERNEL_K2_REG)
         return fail(c, LBM_EINVAL, "kernel K2_REG was removed (slower than K2 wherever K2 applies; DESIGN.md section 5)");
     if (o.kernel == LBM_KERNEL_AA && o.bc == LBM_BC_CAVITY && (o.world > 1 || o.local_slabs > 1) &&
@@ -1378,7 +1544,8 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     // of one copy: larger domains per device).  LBM_MEM_LIMIT_BYTES caps the
     // free memory considered (tests).
     bool use_sc = o.kernel == LBM_KERNEL_K2_SC;
-    if (o.kernel == LBM_KERNEL_AUTO) {
+    c->peer = o.halo == LBM_HALO_PEER;
+    if (o.kernel == LBM_KERNEL_AUTO && !c->peer) {
         size_t freeb = 0, totalb = 0;
         if (cudaMemGetInfo(&freeb, &totalb) != cudaSuccess) {
             cudaGetLastError();
@@ -1420,6 +1587,9 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         s.g.x0 = grank * nxl;
         s.g.nzp = s.plan.nz_pitch;
         s.g.pq = s.plan.plane_q;
+        s.g.gy = s.plan.y_ghost;
+        s.g.zoff = s.plan.z_offset;
+        s.g.org = s.plan.cell0;
         s.g.px = s.plan.plane_x;
         s.g.bc = o.bc;
         s.g.poff = 0;
@@ -1449,10 +1619,17 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         }
         const size_t bytes = size_t(s.g.pmod) * size_t(s.plan.plane_x) * c->esize;
         for (int b = 0; b < (c->sc || o.kernel == LBM_KERNEL_AA ? 1 : 2); ++b) {
-            cudaError_t e = cudaMalloc(&s.buf[b], bytes);
-            if (e != cudaSuccess) {
-                cudaGetLastError();
-                return bail(fail(c, LBM_ENOMEM, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e)));
+            if (c->peer) {  // exportable VMM memory the neighbours map (peer.cu)
+                std::string why;
+                if (!peer::alloc(c->device, bytes, &c->pmine[b], &why))
+                    return bail(fail(c, LBM_ENOMEM, "peer-halo lattice allocation (%zu bytes): %s", bytes, why.c_str()));
+                s.buf[b] = c->pmine[b].va;
+            } else {
+                cudaError_t e = cudaMalloc(&s.buf[b], bytes);
+                if (e != cudaSuccess) {
+                    cudaGetLastError();
+                    return bail(fail(c, LBM_ENOMEM, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e)));
+                }
             }
             // ghosts of wall sides are never read; zero everything once for determinism
             if (cudaMemset(s.buf[b], 0, bytes) != cudaSuccess) return bail(fail(c, LBM_ECUDA, "cudaMemset"));
@@ -1475,6 +1652,10 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
             return bail(fail(c, LBM_ENOMEM, "cudaMalloc staging (%zu bytes)", c->stage_bytes));
         }
     }
+    if (c->peer) {
+        lbm_status st = peer_setup(c);
+        if (st != LBM_OK) return bail(st);
+    }
     if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(c, LBM_ECUDA, "create sync"));
     *out = c;
     return LBM_OK;
@@ -1493,6 +1674,16 @@ void lbm_destroy(lbm_ctx* c) {
     for (auto& ev : c->events) {
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
+    }
+    if (c->peer) {
+        // the neighbours may still store into these buffers: wait until they
+        // completed every phase, then unmap theirs and release ours
+        if (!c->poisoned && peer_wait(c) == LBM_OK) wait_stream(c, c->stream);
+        for (auto& side : c->pnb)
+            for (peer::Alloc& m : side) peer::release(&m);
+        peer::release(&c->pflags);
+        for (peer::Alloc& m : c->pmine) peer::release(&m);
+        for (Slab& s : c->slabs) s.buf[0] = s.buf[1] = nullptr;
     }
     for (Slab& s : c->slabs)
         for (void* b : s.buf)

@@ -90,17 +90,6 @@ __host__ __device__ constexpr int wall_idx(int k, int dim, int sgn) {
     return m;
 }
 
-// periodic z-wrap lanes: position of slot k among the slots whose source
-// wraps for a lane on side 0 (c_z == s or 0) or side 1 (c_z == s), s = +-1
-__host__ __device__ constexpr int zwrap_idx(int k, int side, int s) {
-    int m = 0;
-    for (int j = 0; j < k; ++j) {
-        const int cz = can_cz(slot_dir(j));
-        if (cz == s || (side == 0 && cz == 0)) ++m;
-    }
-    return m;
-}
-
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
                  "l"(src)
@@ -140,26 +129,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         if (spin > (1u << 28)) __trap();
     }
 }
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
-
-// periodic index wrap: one period away without a division (every wrapped
-// K2 source, except in domains narrower than a tile: the % path)
-__device__ __forceinline__ int wrapi(int v, int n) {
-    int w = v < 0 ? v + n : (v >= n ? v - n : v);
-    if (w < 0 || w >= n) {
-        w = v % n;
-        if (w < 0) w += n;
-    }
-    return w;
-}
-
 __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                                  int c2, uint64_t pol) {
     asm volatile(
@@ -171,16 +140,11 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m
 
 }  // namespace
 
-// EXPERIMENT flags (temporary, LBM_EXP env): bit 0 = periodic: skip wrapped
-// sources (wrong results, timing only); bit 1 = TMA loads evict_last;
-// bit 2 = TMA loads evict_first
-__device__ int g_k2_exp = 0;
-
 template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
 __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     k2_sweep(const __grid_constant__ CUtensorMap tmA, const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
              int xbeg, int xend, int chunk, int out_poff, unsigned* __restrict__ sc_sync, T* haloL, T* haloR,
-             int xbeg2, int nch1) {
+             int xbeg2, int nch1, int kflags) {
     using C = K2Cfg<T, TY, TZ>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* const stage = reinterpret_cast<T*>(smem_raw);
@@ -272,22 +236,23 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool edge_y = (y0 < 2) || (y0 + TY + 2 > g.ny);
     const bool edge_z = (z0 < 2) || (z0 + TZ + 2 > g.nz);
 
-    const int exp = g_k2_exp;
-    uint64_t pol = 0;
-    if (exp & 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    if (exp & 4) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    // L2 policy of the staging loads: evict_last (default) keeps the rows a
+    // neighbouring tile or the next plane's CTA re-stages in L2 in preference
+    // to the streaming output (stored evict-first): measured +0.9% on config
+    // 5 fp64 (LBM_K2_EVICT_LAST=0 restores evict_normal)
+    uint64_t pol;
+    if (kflags & 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    // Periodic boxes: the TMA box reads the ghost frame (SlabGeom) instead of
+    // wrapping -- coordinates are frame coordinates, y + gy and z + zoff.
     auto issue = [&](int p, int s) {  // one thread: stage plane p into buffer s
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_expect_tx(&bar[s], C::TX_BYTES);
         static_for<0, kQ>([&](auto kc) {
             constexpr int k = decltype(kc)::value;
             constexpr int i = slot_dir(k);
-            if (exp & 6)
-                tma_load_3d_hint(stage + (s * kQ + k) * C::BOXE, &tmA, &bar[s], z0 - C::ZPAD, y0 - 1 - can_cy(i),
-                                 plane_slot_t<RING>(g, p - can_cx(i)) * kQ + k, pol);
-            else
-                tma_load_3d(stage + (s * kQ + k) * C::BOXE, &tmA, &bar[s], z0 - C::ZPAD, y0 - 1 - can_cy(i),
-                            plane_slot_t<RING>(g, p - can_cx(i)) * kQ + k);
+            tma_load_3d_hint(stage + (s * kQ + k) * C::BOXE, &tmA, &bar[s], z0 - C::ZPAD + g.zoff,
+                             y0 - 1 - can_cy(i) + g.gy, plane_slot_t<RING>(g, p - can_cx(i)) * kQ + k, pol);
         });
     };
 
@@ -351,42 +316,45 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     if (p_first <= p_last) wall_prefetch(p_first, 0);
-    // Periodic z-wrap lanes (fp64 8x32: they fit the wall buffer): in the
-    // first and the last z tile the two edge columns pull 14 / 5 values from
-    // across the z wrap, which the TMA box zero-fills.  They are prefetched
-    // one plane ahead with cp.async like the cavity wall values:
-    // [side 0: HY lanes x 14][side 1: HY lanes x 5] per buffer.
-    // (fp64 only: the ring kernel spills with it; fp32 16x32 would need a
-    // larger buffer, and with one measured 40.5k vs 41.8k MLUPS on config 3)
-    constexpr bool kZPre = BC == BC_PERIODIC && !RING && sizeof(T) == 8 && C::HY * kQ <= C::WALLE;
-    const bool zlo = z0 == 0, zhi = z0 + TZ >= g.nz;
-    const bool zpre = kZPre && zlo != zhi && g.nz % TZ == 0;
-    const int zs = zlo ? 1 : -1;  // c_z of the slots that wrap on side 1
-    const int zside = !zpre || !act1 || (exp & 1) ? -1
-                      : zlo ? (b == 0 ? 0 : (b == 1 ? 1 : -1)) : (b == TZ + 1 ? 0 : (b == TZ ? 1 : -1));
-    auto zwrap_prefetch = [&](int pn, int buf) {
-        if constexpr (kZPre) {
-            if (zside < 0) return;
-            T* const wb = wallbuf + buf * C::WALLE + (zside == 0 ? a * 14 : C::HY * 14 + a * 5);
-            const int sy0 = wrapi(qy, g.ny);
-            static_for<0, kQ>([&](auto kc) {
-                constexpr int k = decltype(kc)::value;
-                constexpr int i = slot_dir(k);
-                constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
-                if (cz == zs || (zside == 0 && cz == 0)) {
-                    const int sy = cy == 0 ? sy0 : wrapi(qy - cy, g.ny);
-                    const T* src = A + plane_base_t<RING>(g, pn - cx) + (long long)k * g.pq +
-                                   (long long)sy * g.nzp + wrapi(qz - cz, g.nz);
-                    T* d = wb + (zs > 0 ? zwrap_idx(k, 0, 1) : zwrap_idx(k, 0, -1));
-                    if (zside == 1) d = wb + (zs > 0 ? zwrap_idx(k, 1, 1) : zwrap_idx(k, 1, -1));
-                    if constexpr (sizeof(T) == 8) cp_async8(d, src);
-                    else cp_async4(d, src);
+    // Periodic ghost-frame copies of this thread's step-2 cell: bits 0-3 =
+    // frame rows -2, -1, ny, ny+1 that hold row y2 (mod ny), bits 4-7 = frame
+    // columns -2, -1, nz, nz+1 that hold column z2 (mod nz).  Written with the
+    // cell's stores, so the next sweep's TMA boxes find the frame complete.
+    int fmask = 0;
+    if constexpr (BC == BC_PERIODIC) {
+        if (in2) {
+            const int yy = y0 + y2, zz = z0 + z2;
+            const int ty[4] = {-2, -1, g.ny, g.ny + 1}, tz[4] = {-2, -1, g.nz, g.nz + 1};
+            for (int j = 0; j < 4; ++j) {
+                if (((ty[j] % g.ny) + g.ny) % g.ny == yy) fmask |= 1 << j;
+                if (((tz[j] % g.nz) + g.nz) % g.nz == zz) fmask |= 16 << j;
+            }
+        }
+    }
+    // the frame copies of a finished step-2 cell into plane buffer D (slot-0
+    // origin; slots where KEEP(k) holds): every (row, column) of {y2 and its
+    // frame rows} x {z2 and its frame columns} except the cell itself
+    auto store_frame = [&](T* D, auto keep, const T (&v)[kQ]) {
+        if constexpr (BC == BC_PERIODIC) {
+            const int yy = y0 + y2, zz = z0 + z2;
+#pragma unroll 1
+            for (int ra = 0; ra < 5; ++ra) {
+                if (ra > 0 && !((fmask >> (ra - 1)) & 1)) continue;
+                const int ry = ra == 0 ? yy : (ra == 1 ? -2 : ra == 2 ? -1 : g.ny + ra - 3);
+#pragma unroll 1
+                for (int cb = 0; cb < 5; ++cb) {
+                    if (cb > 0 && !((fmask >> (3 + cb)) & 1)) continue;
+                    if (ra == 0 && cb == 0) continue;
+                    const int rz = cb == 0 ? zz : (cb == 1 ? -2 : cb == 2 ? -1 : g.nz + cb - 3);
+                    T* const dst = D + (long long)ry * g.nzp + rz;
+                    static_for<0, kQ>([&](auto kc) {
+                        constexpr int k = decltype(kc)::value;
+                        if (keep(k)) __stcs(dst + (long long)k * g.pq, v[slot_dir(k)]);
+                    });
                 }
-            });
-            asm volatile("cp.async.commit_group;" ::: "memory");
+            }
         }
     };
-    if (p_first <= p_last) zwrap_prefetch(p_first, 0);
 
     // Software pipeline, ONE block barrier per plane (after the stage read).
     // Iteration p runs, in the same phase, step 2 of destination plane p-2
@@ -405,31 +373,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         T* const st = stage + s * kQ * C::BOXE;
         const bool lwall = BC == BC_CAVITY && p == 0 && g.left_wall;
         const bool rwall = BC == BC_CAVITY && p == g.nxl - 1 && g.right_wall;
-        // Periodic edge tiles: sources that wrap (outside [0,ny) x [0,nz); the
-        // TMA zero-filled them) are loaded per thread from the wrapped cell
-        // after the stage read (no CTA-wide fix-up pass: measured +9% over
-        // one; issuing them before the stage wait paid only while the wrap
-        // used an integer division).  With zpre the z-wrap lanes take theirs
-        // from the prefetch instead.
         T fs[kQ];
-        const bool wdir = BC == BC_PERIODIC && has1 && (edge_y || (edge_z && !zpre)) && act1 && !(exp & 1);
-        auto wraps = [&](int cy, int cz) {
-            const int sy = qy - cy, sz = qz - cz;
-            const bool zw = sz < 0 || sz >= g.nz;
-            return (sy < 0 || sy >= g.ny || zw) && !(zpre && zw);
-        };
-        auto load_wrapped = [&] {
-            if (wdir) {
-                static_for<0, kQ>([&](auto kc) {
-                    constexpr int k = decltype(kc)::value;
-                    constexpr int i = slot_dir(k);
-                    constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
-                    if (wraps(cy, cz))
-                        fs[i] = A[plane_base_t<RING>(g, p - cx) + (long long)k * g.pq +
-                                  (long long)wrapi(qy - cy, g.ny) * g.nzp + wrapi(qz - cz, g.nz)];
-                });
-            }
-        };
         if (has1) {
             mbar_wait(&bar[s], uint32_t(c >> 1) & 1u);
         }
@@ -447,28 +391,6 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                     constexpr int i = slot_dir(k);
                     fs[i] = sp[k * C::BOXE - can_cz(i)];
                 });
-                if constexpr (BC == BC_PERIODIC) load_wrapped();
-                if constexpr (BC == BC_PERIODIC) {
-                    // z-wrap lanes: their prefetched wrapped values
-                    if constexpr (kZPre) {
-                        if (zside >= 0) {
-                            asm volatile("cp.async.wait_group 0;" ::: "memory");
-                            const T* const wb =
-                                wallbuf + (c & 1) * C::WALLE + (zside == 0 ? a * 14 : C::HY * 14 + a * 5);
-                            static_for<0, kQ>([&](auto kc) {
-                                constexpr int k = decltype(kc)::value;
-                                constexpr int i = slot_dir(k);
-                                constexpr int cz = can_cz(i);
-                                if (cz == zs || (zside == 0 && cz == 0)) {
-                                    const int o = zside == 0 ? (zs > 0 ? zwrap_idx(k, 0, 1) : zwrap_idx(k, 0, -1))
-                                                             : (zs > 0 ? zwrap_idx(k, 1, 1) : zwrap_idx(k, 1, -1));
-                                    fs[i] = wb[o];
-                                }
-                            });
-                        }
-                        if (p + 1 <= p_last) zwrap_prefetch(p + 1, (c + 1) & 1);
-                    }
-                }
                 if constexpr (BC == BC_CAVITY) {
                     // Wall links (source beyond a wall):
                     // the staged entry (TMA zero fill, or a cell beyond the x
@@ -575,6 +497,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 constexpr int k = decltype(kc)::value;
                 __stcs(Bd + (long long)k * g.pq + st_off, f2[slot_dir(k)]);
             });
+            if (fmask && !(kflags & 2)) store_frame(Bd, [](int) { return true; }, f2);
             if constexpr (!RING) {
                 // Fused halo: the planes a neighbouring
                 // slab reads as ghosts also go straight into its next-sweep
@@ -589,6 +512,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                         constexpr int k = decltype(kc)::value;
                         if (d == 0 || k < kSlotsM) __stcs(H + (long long)k * g.pq + st_off, f2[slot_dir(k)]);
                     });
+                    if (fmask) store_frame(H, [d](int k) { return d == 0 || k < kSlotsM; }, f2);
                 }
                 if (d >= g.nxl - 2 && haloR) {
                     T* const H = haloR + (long long)(d - g.nxl + 2) * g.px;
@@ -596,6 +520,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                         constexpr int k = decltype(kc)::value;
                         if (d == g.nxl - 1 || k >= kSlotP0) __stcs(H + (long long)k * g.pq + st_off, f2[slot_dir(k)]);
                     });
+                    if (fmask) store_frame(H, [d, &g](int k) { return d == g.nxl - 1 || k >= kSlotP0; }, f2);
                 }
             }
         }
@@ -759,17 +684,17 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
         if (occ < 1) return cudaErrorInvalidConfiguration;
         occ_cache[dev].store(occ, std::memory_order_release);
     }
-    static const bool exp_set = [] {
-        const char* e = getenv("LBM_EXP");
-        const int v = e ? atoi(e) : 0;
-        return cudaMemcpyToSymbol(g_k2_exp, &v, sizeof v) == cudaSuccess;
-    }();
-    if (!exp_set) return cudaErrorUnknown;
     EncodeFn enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     const SlabGeom& g = P.g;
     CUtensorMap map;
-    const cuuint64_t dims[3] = {cuuint64_t(g.nz), cuuint64_t(g.ny), cuuint64_t(g.pmod) * kQ};
+    // Cavity: the cells only, so boxes reaching past a wall are zero-filled
+    // (the wall lanes substitute those entries).  Periodic: the whole plane
+    // including the ghost frame, from the buffer base (A is the cell origin).
+    const bool frame = g.gy > 0;
+    const T* const base = A - g.org;
+    const cuuint64_t dims[3] = {cuuint64_t(frame ? g.nzp : g.nz), cuuint64_t(g.ny + 2 * g.gy),
+                                cuuint64_t(g.pmod) * kQ};
     const cuuint64_t strides[2] = {cuuint64_t(g.nzp) * sizeof(T), cuuint64_t(g.pq) * sizeof(T)};
     const cuuint32_t box[3] = {cuuint32_t(C::BW), cuuint32_t(C::HY), 1u};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
@@ -784,7 +709,7 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
         return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     }();
     CUresult r = enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-                     const_cast<T*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     const_cast<T*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     // x chunks: fill the machine in whole waves; each chunk re-computes 2 halo planes of step 1
@@ -836,8 +761,13 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
         cudaError_t e = cudaMemsetAsync(sc_sync, 0, sizeof(unsigned) * (1 + grid.y), s);
         if (e != cudaSuccess) return e;
     }
+    static const int l2last = [] {
+        const char* e = getenv("LBM_K2_EVICT_LAST");  // A/B runs: 0 = evict_normal staging loads
+        const char* x = getenv("LBM_EXP_NOFRAME");     // EXPERIMENT (temporary): skip frame stores
+        return ((e && e[0] == '0') ? 0 : 1) | ((x && x[0] == '1') ? 2 : 0);
+    }();
     kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk, out_poff, sc_sync, haloL, haloR, xbeg2,
-                                   nch1);
+                                   nch1, l2last);
     return cudaGetLastError();
 }
 

@@ -42,6 +42,11 @@ int k2_sc_gap();
 template <typename T>
 bool k2_supported(const SlabGeom& g);
 
+// Periodic ghost frame of the slab's own planes [0, nxl) from their cells
+// (F = cell origin); a no-op without a frame (cavity).
+template <typename T>
+cudaError_t launch_frame_fill(T* F, const SlabGeom& g, cudaStream_t s);
+
 // canonical feq of planes [xbeg, xbeg + nxc) (nxc < 0: the whole slab); rho/u
 // point at the first of those planes
 template <typename T>

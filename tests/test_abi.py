@@ -26,7 +26,7 @@ def test_header_symbols_exported():
     for s in syms:
         assert hasattr(L, s), f"{s} declared in include/lbm.h but not exported"
     assert sorted(lbm.EXPORTS) == syms
-    assert lbm.lbm_abi_version() == 1
+    assert lbm.lbm_abi_version() == 2
 
 
 def test_library_is_sm100a():
@@ -82,6 +82,22 @@ def test_create_rejects_bad_kernel_choices():
         lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
 
 
+def test_peer_halo_rejects_unsupported():
+    """LBM_HALO_PEER needs NCCL ranks and the two-buffer K2 storage."""
+    o = lbm.lbm_default_opts()
+    o.halo = lbm.LBM_HALO_PEER
+    with pytest.raises(lbm.LbmError, match="comm NCCL"):
+        lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+    o.comm, o.nccl_id = lbm.LBM_COMM_NCCL, ctypes.cast(ctypes.create_string_buffer(128), ctypes.c_void_p)
+    for k in (lbm.LBM_KERNEL_AA, lbm.LBM_KERNEL_K2_SC, lbm.LBM_KERNEL_K1):
+        o.kernel = k
+        with pytest.raises(lbm.LbmError, match="two-buffer"):
+            lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+    o.kernel, o.halo = 0, 3
+    with pytest.raises(lbm.LbmError, match="bad halo"):
+        lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+
+
 def test_header_enums_match_binding():
     """Every enumerator of include/lbm.h has the same value in the binding."""
     src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "lbm.h")).read(), flags=re.S)
@@ -107,7 +123,9 @@ def test_no_gpu_reports_cuda_error_not_crash():
     assert e.value.status in (3, 2)
 
 
-@pytest.mark.parametrize("dtype,esize,pitch", [("f64", 8, 8), ("f32", 4, 8)])
+# (cavity pitch, periodic pitch): cavity rows padded to 32 B; periodic rows
+# carry the ghost frame -- 32 B before z = 0, >= max(2, 16 B) after nz - 1
+@pytest.mark.parametrize("dtype,esize,pitch", [("f64", 8, (8, 12)), ("f32", 4, (8, 24))])
 def test_halo_plan_layout(dtype, esize, pitch):
     nx, ny, nz = 32, 6, 5
     for world in (1, 2, 4):
@@ -116,8 +134,13 @@ def test_halo_plan_layout(dtype, esize, pitch):
                 p = lbm.lbm_plan_halo(nx, ny, nz, dtype, bc, r, world)
                 nxl = nx // world
                 assert p.nx_local == nxl and p.x0 == r * nxl
-                assert p.nz_pitch == pitch and (p.nz_pitch * esize) % 32 == 0
-                assert p.plane_q == ny * p.nz_pitch and p.plane_x == 19 * p.plane_q
+                per = bc == lbm.LBM_BC_PERIODIC
+                assert p.nz_pitch == pitch[per] and (p.nz_pitch * esize) % 32 == 0
+                assert (p.y_ghost, p.z_offset) == ((2, 32 // esize) if per else (0, 0))
+                assert p.cell0 == p.y_ghost * p.nz_pitch + p.z_offset
+                assert (p.z_offset * esize) % 32 == 0  # cells stay 32 B aligned
+                assert p.nz_pitch - p.z_offset - nz >= (max(2, 16 // esize) if per else 0)
+                assert p.plane_q == (ny + 2 * p.y_ghost) * p.nz_pitch and p.plane_x == 19 * p.plane_q
                 assert p.buffer_elems == (nxl + 4) * p.plane_x
                 assert p.span == 24 * p.plane_q
                 # spans stay inside the buffer and the ghost spans stay inside ghost planes

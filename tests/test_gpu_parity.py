@@ -215,6 +215,28 @@ def test_k2_equals_k1_bitwise(dims, bc, dtype):
     assert relerr_floor(res[lbm.LBM_KERNEL_K2], oracle.run(f0, bc, 0.6, LID, 4)) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("dims", [(4, 1, 1), (4, 2, 3), (5, 3, 2), (6, 1, 37), (4, 9, 1), (6, 4, 33), (4, 17, 64)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("kernel", ["k2", "k2sc"])
+def test_periodic_frame_bitwise(dims, dtype, kernel):
+    """Periodic boxes read the ghost frame: K2 keeps it
+    current with its stores (a row / column may have several frame copies
+    when ny or nz < 4), and after a K1 step or an import the frame is
+    rebuilt before the next K2 sweep.  Bitwise equal to K1 for step splits
+    that alternate the two, and to the oracle."""
+    f0 = li.random_populations(35, *dims)
+    kern = lbm.LBM_KERNEL_K2 if kernel == "k2" else lbm.LBM_KERNEL_K2_SC
+    res = []
+    for k, splits in ((lbm.LBM_KERNEL_K1, [10]), (kern, [1, 2, 3, 2, 2])):
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=lbm.LBM_BC_PERIODIC, kernel=k) as lat:
+            lat.set_populations(f0)
+            for n in splits:
+                lat.step(n)
+            res.append(lat.populations())
+    assert np.array_equal(res[0], res[1])
+    assert relerr_floor(res[1], oracle.run(f0, lbm.LBM_BC_PERIODIC, 0.6, LID, 10)) <= TOL[dtype] * 10
+
+
 K2_VARIANTS = [("LBM_K2_TILE", v, 2) for v in ["8x32", "8x16", "16x16"]] + [("LBM_K2_EARLY", "0", 2), ("LBM_K2_CHUNK", "3", 2)]
 
 
@@ -384,6 +406,38 @@ def test_aa_local_slabs_bitwise(bc, slabs, dtype):
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
     assert relerr_floor(runs[1][-1][0], oracle.run(f0, bc, 0.6, LID, 7)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_peer_halo_world1_self_import_bitwise(dtype):
+    """The fused cross-GPU halo (LBM_HALO_PEER) as a
+    one-rank periodic ring: the lattice buffers are exported as file
+    descriptors, passed over the rendezvous socket to this rank itself and
+    mapped a second time; K2 stores the x ghost planes through that mapping
+    as it would into a neighbour's memory over NVLink, and consecutive
+    sweeps wait on the done-counter the previous sweep wrote through it
+    (stream memory operations).  Odd splits (K1 steps through NCCL) and
+    read-backs between sweeps; bitwise equal to the in-process wrap."""
+    dims = (24, 10, 36)
+    f0 = li.random_populations(57, *dims)
+    try:
+        uid = lbm.lbm_nccl_unique_id()
+    except lbm.LbmError as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    outs = []
+    for kw in ({}, dict(comm=lbm.LBM_COMM_NCCL, nccl_id=uid, halo=lbm.LBM_HALO_PEER)):
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=lbm.LBM_BC_PERIODIC, **kw) as lat:
+            lat.set_populations(f0)
+            out = []
+            for n in (3, 2, 4, 1, 2):
+                lat.step(n)
+                out.append(lat.populations())
+                out.extend(lat.macroscopic())
+            st = lbm.lbm_get_stats(lat.ctx)
+            outs.append((out, st.launches))
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert np.array_equal(a, b)
+    assert relerr_floor(outs[1][0][-3], oracle.run(f0, lbm.LBM_BC_PERIODIC, 0.6, LID, 12)) <= TOL[dtype] * 4
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])

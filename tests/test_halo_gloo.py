@@ -37,18 +37,20 @@ def to_buffer(G, p, x0, nxl):
     ghosts NaN) in the library layout described by plan p."""
     _, nx, ny, nz = G.shape
     buf = np.full(p.buffer_elems, np.nan)
-    v = buf.reshape(nxl + 4, 19, ny, p.nz_pitch)
+    v = buf.reshape(nxl + 4, 19, p.plane_q // p.nz_pitch, p.nz_pitch)
+    gy, zo = p.y_ghost, p.z_offset
     for k in range(19):
-        v[2:nxl + 2, k, :, :nz] = G[p.dir_of_slot[k], x0:x0 + nxl]
+        v[2:nxl + 2, k, gy:gy + ny, zo:zo + nz] = G[p.dir_of_slot[k], x0:x0 + nxl]
     return buf
 
 
 def from_buffer(buf, p, nxl, ny, nz):
     """Slab buffer -> canonical A[19, nxl + 4, ny, nz] (ghost planes included)."""
-    v = buf.reshape(nxl + 4, 19, ny, p.nz_pitch)
+    v = buf.reshape(nxl + 4, 19, p.plane_q // p.nz_pitch, p.nz_pitch)
+    gy, zo = p.y_ghost, p.z_offset
     A = np.empty((19, nxl + 4, ny, nz))
     for k in range(19):
-        A[p.dir_of_slot[k]] = v[:, k, :, :nz]
+        A[p.dir_of_slot[k]] = v[:, k, gy:gy + ny, zo:zo + nz]
     return A
 
 
