@@ -339,18 +339,20 @@ def main():
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "MLUPS", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
 
-    # roofline.traffic: measured DRAM bytes per sweep launch from the committed
-    # ncu capture of this workload/dtype/kernel (profiles/r01_traffic.json), if any
+    # roofline.traffic: measured DRAM bytes per sweep launch from the newest
+    # committed ncu capture of this workload/dtype/kernel (profiles/rNN_traffic.json)
     traffic = None
-    try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        t = tj.get(cfg.name, {}).get(dominant, {}).get(args.dtype) if world == 1 else None
-        if t:
-            traffic = {"bytes_per_launch": t["read"] + t["write"], "read": t["read"], "write": t["write"],
-                       "x_algorithmic": round((t["read"] + t["write"]) / bytes_per_launch, 3),
-                       "source": "profiles/r01_traffic.json (ncu --set full, same workload)"}
-    except (OSError, ValueError, KeyError):
-        traffic = None
+    for tf in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", tf)))
+            t = tj.get(cfg.name, {}).get(dominant, {}).get(args.dtype) if world == 1 else None
+            if t:
+                traffic = {"bytes_per_launch": t["read"] + t["write"], "read": t["read"], "write": t["write"],
+                           "x_algorithmic": round((t["read"] + t["write"]) / bytes_per_launch, 3),
+                           "source": f"profiles/{tf} (ncu --set full, same workload)"}
+                break
+        except (OSError, ValueError, KeyError):
+            continue
 
     if rank == 0:
         mlups_bytes = 2 * 19 * es  # BASELINE.json:5 roofline: MLUPS x single-step bytes / peak

@@ -264,9 +264,10 @@ typedef struct {
     int dir_of_slot[19];     /* canonical direction stored at internal slot k */
     /* Periodic boxes: every (x, direction) plane has a ghost frame of
      * y_ghost (2) rows above and below the ny rows and z_offset elements
-     * (32 bytes) before z = 0 (>= 2 after z = nz-1), holding copies of the
-     * periodically wrapped cells; cavity: 0, 0.  Cell (y, z) of a plane is at
-     * cell0 + y * nz_pitch + z, cell0 = y_ghost * nz_pitch + z_offset. */
+     * (32 bytes) of columns before z = 0 and after z = nz-1, holding copies
+     * of the periodically wrapped cells; cavity: 0, 0.  Cell (y, z) of a
+     * plane is at cell0 + y * nz_pitch + z, cell0 = y_ghost * nz_pitch +
+     * z_offset. */
     int y_ghost, z_offset;
     long long cell0;
 } lbm_halo_plan;

@@ -318,13 +318,14 @@ void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world
     p->nx_local = nxl;
     p->x0 = x0;
     // rows start on 32 B sectors.  Periodic: the ghost frame (SlabGeom) --
-    // 2 rows per side, 32 B of columns before z = 0 (so the cells stay
-    // sector aligned) and >= max(2, 16 B) after nz - 1 (K2's TMA box reach)
+    // 2 rows per side and a 32 B sector of columns before z = 0 and after
+    // nz - 1 (the cells stay sector aligned; K2's TMA box reaches 16 B and
+    // >= 2 cells beyond the tile)
     const int sector = int(32 / esize);
     if (bc == LBM_BC_PERIODIC) {
         p->y_ghost = 2;
         p->z_offset = sector;
-        p->nz_pitch = round_up(sector + nz + std::max(2, int(16 / esize)), sector);
+        p->nz_pitch = round_up(sector + nz + sector, sector);
     } else {
         p->y_ghost = 0;
         p->z_offset = 0;

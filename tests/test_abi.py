@@ -124,8 +124,8 @@ def test_no_gpu_reports_cuda_error_not_crash():
 
 
 # (cavity pitch, periodic pitch): cavity rows padded to 32 B; periodic rows
-# carry the ghost frame -- 32 B before z = 0, >= max(2, 16 B) after nz - 1
-@pytest.mark.parametrize("dtype,esize,pitch", [("f64", 8, (8, 12)), ("f32", 4, (8, 24))])
+# carry the ghost frame -- a 32 B sector before z = 0 and after nz - 1
+@pytest.mark.parametrize("dtype,esize,pitch", [("f64", 8, (8, 16)), ("f32", 4, (8, 24))])
 def test_halo_plan_layout(dtype, esize, pitch):
     nx, ny, nz = 32, 6, 5
     for world in (1, 2, 4):
@@ -139,7 +139,7 @@ def test_halo_plan_layout(dtype, esize, pitch):
                 assert (p.y_ghost, p.z_offset) == ((2, 32 // esize) if per else (0, 0))
                 assert p.cell0 == p.y_ghost * p.nz_pitch + p.z_offset
                 assert (p.z_offset * esize) % 32 == 0  # cells stay 32 B aligned
-                assert p.nz_pitch - p.z_offset - nz >= (max(2, 16 // esize) if per else 0)
+                assert p.nz_pitch - p.z_offset - nz >= (32 // esize if per else 0)
                 assert p.plane_q == (ny + 2 * p.y_ghost) * p.nz_pitch and p.plane_x == 19 * p.plane_q
                 assert p.buffer_elems == (nxl + 4) * p.plane_x
                 assert p.span == 24 * p.plane_q
