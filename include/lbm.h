@@ -138,7 +138,16 @@ typedef enum {
      * set_populations write the canonical state and invert the stream in
      * place.  EINVAL at create where the TMA descriptor cannot describe the
      * slab. */
-    LBM_KERNEL_K2_SC = 5
+    LBM_KERNEL_K2_SC = 5,
+    /* Three collision-streaming steps per HBM pass (
+     * the paper's future work "merge more time steps"):
+     * the K2 sweep one level deeper -- T+2 staged, two shared-memory rings --
+     * so each population crosses HBM once per three steps, for 1.69 + 1.33
+     * + 1 collisions per output cell.  A measured prototype (DESIGN.md
+     * section 11): fp32, periodic, one slab (comm NONE); EINVAL otherwise.
+     * lbm_step(n) runs floor(n/3) three-step sweeps, the remainder as K2 /
+     * K1.  Bitwise identical to K1. */
+    LBM_KERNEL_K3 = 6
 } lbm_kernel;
 
 /* Halo transport between X-slabs (PAPER.md:336 X-only partition).
@@ -263,7 +272,7 @@ typedef struct {
     long long span;          /* elements per message (24 * plane_q) */
     int dir_of_slot[19];     /* canonical direction stored at internal slot k */
     /* Periodic boxes: every (x, direction) plane has a ghost frame of
-     * y_ghost (2) rows above and below the ny rows and z_offset elements
+     * y_ghost (3) rows above and below the ny rows and z_offset elements
      * (32 bytes) of columns before z = 0 and after z = nz-1, holding copies
      * of the periodically wrapped cells; cavity: 0, 0.  Cell (y, z) of a
      * plane is at cell0 + y * nz_pitch + z, cell0 = y_ghost * nz_pitch +

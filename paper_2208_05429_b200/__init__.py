@@ -28,6 +28,7 @@ LIB_PATH = _build.LIB
 LBM_F64, LBM_F32 = 0, 1
 LBM_BC_CAVITY, LBM_BC_PERIODIC = 0, 1
 LBM_KERNEL_AUTO, LBM_KERNEL_K1, LBM_KERNEL_K2, LBM_KERNEL_K2_REG, LBM_KERNEL_AA, LBM_KERNEL_K2_SC = 0, 1, 2, 3, 4, 5
+LBM_KERNEL_K3 = 6
 LBM_COMM_NONE, LBM_COMM_NCCL, LBM_COMM_LOCAL = 0, 1, 2
 LBM_HALO_AUTO, LBM_HALO_EXCHANGE, LBM_HALO_PEER = 0, 1, 2
 LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_ESTATE, LBM_ENUMERIC = 0, 1, 2, 3, 4, 5, 6

@@ -317,13 +317,14 @@ void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world
     memset(p, 0, sizeof *p);
     p->nx_local = nxl;
     p->x0 = x0;
-    // rows start on 32 B sectors.  Periodic: the ghost frame (SlabGeom) --
-    // 2 rows per side and a 32 B sector of columns before z = 0 and after
-    // nz - 1 (the cells stay sector aligned; K2's TMA box reaches 16 B and
-    // >= 2 cells beyond the tile)
+    // rows start on 32 B sectors.  Periodic: the ghost frame (SlabGeom,
+    // frame.cuh) -- 3 rows per side (the three-step sweep's reach) and a
+    // 32 B sector of columns before z = 0 and after nz - 1 (the cells stay
+    // sector aligned; K2's / K3's TMA boxes reach 16 B and <= 3 cells beyond
+    // the tile)
     const int sector = int(32 / esize);
     if (bc == LBM_BC_PERIODIC) {
-        p->y_ghost = 2;
+        p->y_ghost = 3;
         p->z_offset = sector;
         p->nz_pitch = round_up(sector + nz + sector, sector);
     } else {
@@ -735,10 +736,40 @@ lbm_status sc_finish_canonical(lbm_ctx* c) {
     return LBM_OK;
 }
 
+// Three-step sweeps (K3, k3.cu): floor(n/3) of them; the caller runs the
+// remainder.  K3 reads no ghost plane (it wraps the plane index itself) but
+// writes none either, so afterwards the ghosts are stale.
+template <typename T>
+lbm_status run_steps_k3(lbm_ctx* c, long& n) {
+    while (n >= 3) {
+        lbm_status st = ensure_frame<T>(c, c->cur);
+        if (st != LBM_OK) return st;
+        size_t slot = 0;
+        if ((st = prof_begin(c, slot)) != LBM_OK) return st;
+        Slab& s = c->slabs[0];
+        cudaError_t e = launch_k3<T>(origin<T>(s, c->cur), origin<T>(s, c->cur ^ 1), make_params<T>(c, s), c->stream);
+        if (e != cudaSuccess) return fail(c, LBM_ECUDA, "K3 sweep launch failed: %s", cudaGetErrorString(e));
+        c->launches++;
+        c->k2_launches++;
+        if ((st = prof_end(c, slot, 3LL * s.g.nxl * s.g.ny * s.g.nz)) != LBM_OK) return st;
+        c->cur ^= 1;
+        c->ghosts_valid = false;
+        c->frame_valid = true;
+        c->t += 3;
+        n -= 3;
+    }
+    return LBM_OK;
+}
+
 template <typename T>
 lbm_status run_steps(lbm_ctx* c, long n) {
     if (c->aa) return run_steps_aa<T>(c, n);
     if (c->sc) return run_steps_sc<T>(c, n);
+    if (c->opts.kernel == LBM_KERNEL_K3) {
+        if (!k3_supported<T>(c->slabs[0].g)) return fail(c, LBM_EINVAL, "kernel K3 not supported for this slab");
+        lbm_status st = run_steps_k3<T>(c, n);
+        if (st != LBM_OK) return st;
+    }
     // AUTO and K2: the TMA-staged two-step sweep (k2.cu) where the TMA
     // descriptor can describe the slab; AUTO falls back to K1 pairs where it
     // cannot, an explicit K2 request then fails.
@@ -1451,7 +1482,10 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         return fail(c, LBM_EINVAL, "comm NCCL needs local_slabs == 1 and an nccl_id");
     if (o.comm == LBM_COMM_LOCAL && o.world != 1) return fail(c, LBM_EINVAL, "comm LOCAL needs world == 1");
     if (o.comm < LBM_COMM_NONE || o.comm > LBM_COMM_LOCAL) return fail(c, LBM_EINVAL, "bad comm %d", o.comm);
-    if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K2_SC) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    if (o.kernel < LBM_KERNEL_AUTO || o.kernel > LBM_KERNEL_K3) return fail(c, LBM_EINVAL, "bad kernel %d", o.kernel);
+    if (o.kernel == LBM_KERNEL_K3 &&
+        (dt != LBM_F32 || o.bc != LBM_BC_PERIODIC || o.comm != LBM_COMM_NONE))
+        return fail(c, LBM_EINVAL, "kernel K3 (three-step prototype) needs fp32, a periodic box and comm NONE");
     if (o.halo < LBM_HALO_AUTO || o.halo > LBM_HALO_PEER) return fail(c, LBM_EINVAL, "bad halo %d", o.halo);
     if (o.halo == LBM_HALO_PEER && o.comm != LBM_COMM_NCCL)
         return fail(c, LBM_EINVAL, "halo PEER needs comm NCCL (world 1: the periodic self-wrap)");

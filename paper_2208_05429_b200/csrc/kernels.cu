@@ -91,22 +91,22 @@ __global__ void __launch_bounds__(256) k1_step_sc(T* F, StepParams<T> P, int out
 }
 
 // ---------------------------------------------------------- frame fill --
-// Periodic ghost frame (SlabGeom) of the slab's own planes, from their cells:
-// rows -2, -1, ny, ny+1 over z in [-S, nz + S) and the columns [-S, 0) and
-// [nz, nz + S) over y in [0, ny) (S = g.zoff, 32 B of elements), each a copy
-// of the cell (y mod ny, z mod nz).  Run where a writer other than K2 (init,
-// import, K1) left the frame stale; K2 keeps it current itself.  Every
-// source is an interior cell, so the copies are independent.
+// Periodic ghost frame (SlabGeom, frame.cuh) of the slab's own planes, from
+// their cells: rows [-gy, 0) and [ny, ny + gy) over z in [-S, nz + S) and
+// the columns [-S, 0) and [nz, nz + S) over y in [0, ny) (S = g.zoff), each
+// a copy of the cell (y mod ny, z mod nz).  Run where a writer other than
+// K2/K3 (init, import, K1) left the frame stale; the sweeps keep it current
+// themselves.  Every source is an interior cell: the copies are independent.
 template <typename T>
 __global__ void __launch_bounds__(256) k_frame_fill(T* __restrict__ F, SlabGeom g) {
     const int x = int(blockIdx.y) / kQ, k = int(blockIdx.y) % kQ;
     T* const P = F + plane_base(g, x) + (long long)k * g.pq;
-    const int S = g.zoff, W = g.nz + 2 * S, nrow = 4 * W, n = nrow + 2 * S * g.ny;
+    const int S = g.zoff, W = g.nz + 2 * S, nrow = 2 * g.gy * W, n = nrow + 2 * S * g.ny;
     for (int e = int(blockIdx.x * blockDim.x + threadIdx.x); e < n; e += int(gridDim.x * blockDim.x)) {
         int y, z;
         if (e < nrow) {
             const int r = e / W;
-            y = r < 2 ? r - 2 : g.ny + r - 2;
+            y = r < g.gy ? r - g.gy : g.ny + r - g.gy;
             z = e % W - S;
         } else {
             const int q = e - nrow, cidx = q % (2 * S);
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) k_frame_fill(T* __restrict__ F, SlabGeom 
 template <typename T>
 cudaError_t launch_frame_fill(T* F, const SlabGeom& g, cudaStream_t s) {
     if (g.gy == 0 || g.nxl <= 0) return cudaSuccess;
-    const int n = 4 * (g.nz + 2 * g.zoff) + 2 * g.zoff * g.ny;
+    const int n = 2 * g.gy * (g.nz + 2 * g.zoff) + 2 * g.zoff * g.ny;
     k_frame_fill<T><<<dim3(unsigned((n + 255) / 256), unsigned(g.nxl * kQ)), 256, 0, s>>>(F, g);
     return cudaGetLastError();
 }

@@ -47,6 +47,13 @@ bool k2_supported(const SlabGeom& g);
 template <typename T>
 cudaError_t launch_frame_fill(T* F, const SlabGeom& g, cudaStream_t s);
 
+// K3 (k3.cu): three fused steps per HBM pass, A = f*(t-1) -> B = f*(t+2),
+// the whole slab; fp32, periodic, one slab spanning x (k3_supported).
+template <typename T>
+bool k3_supported(const SlabGeom& g);
+template <typename T>
+cudaError_t launch_k3(const T* A, T* B, const StepParams<T>& P, cudaStream_t s);
+
 // canonical feq of planes [xbeg, xbeg + nxc) (nxc < 0: the whole slab); rho/u
 // point at the first of those planes
 template <typename T>

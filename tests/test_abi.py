@@ -71,7 +71,7 @@ def test_create_rejects_bad_partitions():
 
 def test_create_rejects_bad_kernel_choices():
     o = lbm.lbm_default_opts()
-    o.kernel = 6
+    o.kernel = 7
     with pytest.raises(lbm.LbmError, match="bad kernel"):
         lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
     o.kernel = -1
@@ -96,6 +96,20 @@ def test_peer_halo_rejects_unsupported():
     o.kernel, o.halo = 0, 3
     with pytest.raises(lbm.LbmError, match="bad halo"):
         lbm.lbm_create_ex(16, 4, 4, 0.6, None, "f64", o)
+
+
+def test_k3_rejects_unsupported():
+    """The three-step prototype K3 runs fp32 periodic single-slab boxes only."""
+    o = lbm.lbm_default_opts()
+    o.kernel, o.bc = lbm.LBM_KERNEL_K3, lbm.LBM_BC_PERIODIC
+    with pytest.raises(lbm.LbmError, match="K3"):
+        lbm.lbm_create_ex(8, 8, 32, 0.6, None, "f64", o)
+    o.bc = lbm.LBM_BC_CAVITY
+    with pytest.raises(lbm.LbmError, match="K3"):
+        lbm.lbm_create_ex(8, 8, 32, 0.6, None, "f32", o)
+    o.bc, o.comm, o.local_slabs = lbm.LBM_BC_PERIODIC, lbm.LBM_COMM_LOCAL, 2
+    with pytest.raises(lbm.LbmError, match="K3"):
+        lbm.lbm_create_ex(16, 8, 32, 0.6, None, "f32", o)
 
 
 def test_header_enums_match_binding():
@@ -136,7 +150,7 @@ def test_halo_plan_layout(dtype, esize, pitch):
                 assert p.nx_local == nxl and p.x0 == r * nxl
                 per = bc == lbm.LBM_BC_PERIODIC
                 assert p.nz_pitch == pitch[per] and (p.nz_pitch * esize) % 32 == 0
-                assert (p.y_ghost, p.z_offset) == ((2, 32 // esize) if per else (0, 0))
+                assert (p.y_ghost, p.z_offset) == ((3, 32 // esize) if per else (0, 0))
                 assert p.cell0 == p.y_ghost * p.nz_pitch + p.z_offset
                 assert (p.z_offset * esize) % 32 == 0  # cells stay 32 B aligned
                 assert p.nz_pitch - p.z_offset - nz >= (32 // esize if per else 0)

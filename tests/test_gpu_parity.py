@@ -237,6 +237,29 @@ def test_periodic_frame_bitwise(dims, dtype, kernel):
     assert relerr_floor(res[1], oracle.run(f0, lbm.LBM_BC_PERIODIC, 0.6, LID, 10)) <= TOL[dtype] * 10
 
 
+@pytest.mark.parametrize("dims", [(4, 1, 1), (5, 3, 2), (9, 17, 45), (16, 8, 32), (33, 24, 64), (6, 13, 100)])
+def test_k3_three_step_bitwise(dims):
+    """The three-step prototype K3: T+2 staged by TMA,
+    two shared-memory rings, the y/z wrap from the 3-row ghost frame and the
+    x wrap on the TMA plane index -- bit for bit K1 for step counts that mix
+    K3 sweeps with K2 / K1 remainders and read-backs, and the oracle."""
+    f0 = li.random_populations(39, *dims)
+    res = []
+    for k, splits in ((lbm.LBM_KERNEL_K1, [3, 4, 5, 3, 1]), (lbm.LBM_KERNEL_K3, [3, 4, 5, 3, 1])):
+        with lbm.Lattice(*dims, 0.6, LID, "f32", bc=lbm.LBM_BC_PERIODIC, kernel=k) as lat:
+            lat.set_populations(f0)
+            out = []
+            for n in splits:
+                lat.step(n)
+                out.append(lat.populations())
+            res.append(out)
+            st = lbm.lbm_get_stats(lat.ctx)
+    assert st.k2_launches >= 5  # K3 sweeps (counted as multi-step sweeps) ran
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+    assert relerr_floor(res[1][-1], oracle.run(f0, lbm.LBM_BC_PERIODIC, 0.6, LID, 16)) <= TOL["f32"] * 16
+
+
 K2_VARIANTS = [("LBM_K2_TILE", v, 2) for v in ["8x32", "8x16", "16x16"]] + [("LBM_K2_EARLY", "0", 2), ("LBM_K2_CHUNK", "3", 2)]
 
 

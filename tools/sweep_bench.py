@@ -28,7 +28,7 @@ ap.add_argument("--slabs", type=int, default=1, help="LOCAL X-slabs on this GPU 
 ap.add_argument("--power", action="store_true", help="also sample SM clock and board power (NVML)")
 a = ap.parse_args()
 nx, ny, nz = (int(v) for v in a.dims.split(","))
-kern = {"auto": 0, "k1": 1, "k2": 2, "aa": 4, "k2sc": 5}[a.kernel]
+kern = {"auto": 0, "k1": 1, "k2": 2, "aa": 4, "k2sc": 5, "k3": 6}[a.kernel]
 bc = lbm.LBM_BC_CAVITY if a.bc == "cavity" else lbm.LBM_BC_PERIODIC
 es = 8 if a.dtype == "f64" else 4
 kw = dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=a.slabs) if a.slabs > 1 else {}
