@@ -272,7 +272,8 @@ typedef struct {
     long long span;          /* elements per message (24 * plane_q) */
     int dir_of_slot[19];     /* canonical direction stored at internal slot k */
     /* Periodic boxes: every (x, direction) plane has a ghost frame of
-     * y_ghost (3) rows above and below the ny rows and z_offset elements
+     * y_ghost (2; 3 in a LBM_KERNEL_K3 context) rows above and below the ny
+     * rows and z_offset elements
      * (32 bytes) of columns before z = 0 and after z = nz-1, holding copies
      * of the periodically wrapped cells; cavity: 0, 0.  Cell (y, z) of a
      * plane is at cell0 + y * nz_pitch + z, cell0 = y_ghost * nz_pitch +

@@ -312,19 +312,21 @@ lbm_status peer_signal(lbm_ctx* c) {
 }
 
 
+// ghost_rows: periodic frame rows per side -- 2 (K2's reach), 3 for the
+// three-step K3 (a K3 context's own plan; lbm_plan_halo describes K2's)
 void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world, int nxl, int x0,
-               lbm_halo_plan* p) {
+               lbm_halo_plan* p, int ghost_rows = 2) {
     memset(p, 0, sizeof *p);
     p->nx_local = nxl;
     p->x0 = x0;
     // rows start on 32 B sectors.  Periodic: the ghost frame (SlabGeom,
-    // frame.cuh) -- 3 rows per side (the three-step sweep's reach) and a
-    // 32 B sector of columns before z = 0 and after nz - 1 (the cells stay
-    // sector aligned; K2's / K3's TMA boxes reach 16 B and <= 3 cells beyond
-    // the tile)
+    // frame.cuh) -- 2 rows per side (K2's reach; 3 for K3) and a 32 B
+    // sector of columns before z = 0 and after nz - 1 (the cells stay sector
+    // aligned; the TMA boxes reach 16 B and <= 3 cells beyond the tile, and
+    // whole-sector column copies need no L2 fill)
     const int sector = int(32 / esize);
     if (bc == LBM_BC_PERIODIC) {
-        p->y_ghost = 3;
+        p->y_ghost = ghost_rows;
         p->z_offset = sector;
         p->nz_pitch = round_up(sector + nz + sector, sector);
     } else {
@@ -1614,7 +1616,8 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     for (int j = 0; j < sw; ++j) {
         Slab& s = c->slabs[j];
         const int grank = o.rank * sw + j;  // global slab index
-        fill_plan(nx, ny, nz, c->esize, o.bc, grank, nslab_total, nxl, grank * nxl, &s.plan);
+        fill_plan(nx, ny, nz, c->esize, o.bc, grank, nslab_total, nxl, grank * nxl, &s.plan,
+                  o.kernel == LBM_KERNEL_K3 ? 3 : 2);
         s.g.nx = nx;
         s.g.ny = ny;
         s.g.nz = nz;

@@ -21,7 +21,7 @@
 // Scope of the prototype: fp32 (fp64 needs twice the shared memory: no
 // tile fits 227 KB), a periodic box held by one slab (no walls; the x wrap
 // is applied to the TMA plane coordinate, the y/z wrap comes from the ghost
-// frame, which therefore has 3 rows per side -- frame.cuh).  Same
+// frame, which therefore has 3 rows per side in a K3 context -- frame.cuh).  Same
 // bgk_collide() as K1/K2: K3 == K1 o K1 o K1 bit for bit.
 #include <cuda.h>
 

@@ -150,7 +150,7 @@ def test_halo_plan_layout(dtype, esize, pitch):
                 assert p.nx_local == nxl and p.x0 == r * nxl
                 per = bc == lbm.LBM_BC_PERIODIC
                 assert p.nz_pitch == pitch[per] and (p.nz_pitch * esize) % 32 == 0
-                assert (p.y_ghost, p.z_offset) == ((3, 32 // esize) if per else (0, 0))
+                assert (p.y_ghost, p.z_offset) == ((2, 32 // esize) if per else (0, 0))
                 assert p.cell0 == p.y_ghost * p.nz_pitch + p.z_offset
                 assert (p.z_offset * esize) % 32 == 0  # cells stay 32 B aligned
                 assert p.nz_pitch - p.z_offset - nz >= (32 // esize if per else 0)
