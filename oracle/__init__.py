@@ -19,6 +19,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 SRC = os.path.join(HERE, "oracle.c")
+SRCS = [SRC, os.path.join(HERE, "oracle_dqq.c")]
 
 BC_CAVITY = 0
 BC_PERIODIC = 1
@@ -29,12 +30,12 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile liboracle.so: -O2 -ffp-contract=off, no fast-math, OpenMP."""
     stale = (not os.path.exists(LIB_PATH)
-             or os.path.getmtime(LIB_PATH) < max(os.path.getmtime(SRC),
-                                                  os.path.getmtime(os.path.join(HERE, "oracle.h"))))
+             or os.path.getmtime(LIB_PATH) < max([os.path.getmtime(f) for f in SRCS]
+                                                 + [os.path.getmtime(os.path.join(HERE, "oracle.h"))]))
     if force or stale:
         tmp = LIB_PATH + f".tmp{os.getpid()}"
         cmd = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math",
-               "-fopenmp", "-fPIC", "-shared", SRC, "-o", tmp, "-lm"]
+               "-fopenmp", "-fPIC", "-shared", *SRCS, "-o", tmp, "-lm"]
         subprocess.check_call(cmd, cwd=HERE)
         os.replace(tmp, LIB_PATH)
     return LIB_PATH
@@ -59,6 +60,13 @@ def lib():
         L.oracle_step_box.argtypes = ([ctypes.c_int] * 4 + [ctypes.c_double, dp]
                                       + [ctypes.c_int] * 6 + [dp, dp])
         L.oracle_macroscopic.argtypes = [ctypes.c_int] * 3 + [dp, dp, dp]
+        L.oracle_dqq_table.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), dp, ctypes.POINTER(ctypes.c_int)]
+        L.oracle_dqq_table.restype = ctypes.c_int
+        L.oracle_dqq_equilibrium.argtypes = [ctypes.c_int, ctypes.c_double, dp, dp]
+        L.oracle_dqq_collide.argtypes = [ctypes.c_int, dp, ctypes.c_double, dp]
+        L.oracle_dqq_collide.restype = ctypes.c_int
+        L.oracle_dqq_run.argtypes = [ctypes.c_int] * 5 + [ctypes.c_double, dp, ctypes.c_long, dp]
+        L.oracle_dqq_run.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_get_threads.restype = ctypes.c_int
         _lib = L
@@ -164,6 +172,53 @@ def macroscopic(f):
     u = np.zeros((nx, ny, nz, 3))
     lib().oracle_macroscopic(nx, ny, nz, _p(f), _p(rho), _p(u))
     return rho, u
+
+
+# ---- other cubic lattices (oracle_dqq.c): q = 15, 19, 27 ----
+def dqq_table(q: int):
+    """(c[q,3] int, w[q] float64, opp[q] int) of the q-velocity lattice."""
+    c = (ctypes.c_int * (3 * q))()
+    w = np.zeros(q)
+    opp = (ctypes.c_int * q)()
+    if lib().oracle_dqq_table(q, c, _p(w), opp):
+        raise ValueError(f"unsupported lattice D3Q{q}")
+    return np.array(list(c), dtype=np.int64).reshape(q, 3), w, np.array(list(opp), dtype=np.int64)
+
+
+def dqq_equilibrium(q: int, rho: float, u) -> np.ndarray:
+    out = np.zeros(q)
+    lib().oracle_dqq_equilibrium(q, float(rho), _p(_vec3(u)), _p(out))
+    return out
+
+
+def dqq_collide(q: int, f, omega: float) -> np.ndarray:
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    out = np.zeros(q)
+    if lib().oracle_dqq_collide(q, _p(f), float(omega), _p(out)):
+        raise ZeroDivisionError("degenerate moments: rho == 0")
+    return out
+
+
+def dqq_init_equilibrium(q: int, nx, ny, nz, rho=None, u=None) -> np.ndarray:
+    """feq of every cell (plain loop over dqq_equilibrium's C routine)."""
+    f = np.zeros((q, nx, ny, nz))
+    r = np.ones((nx, ny, nz)) if rho is None else np.asarray(rho, dtype=np.float64).reshape(nx, ny, nz)
+    v = np.zeros((nx, ny, nz, 3)) if u is None else np.asarray(u, dtype=np.float64).reshape(nx, ny, nz, 3)
+    for x in range(nx):
+        for y in range(ny):
+            for z in range(nz):
+                f[:, x, y, z] = dqq_equilibrium(q, r[x, y, z], v[x, y, z])
+    return f
+
+
+def dqq_run(q: int, f, bc: int, tau: float, u_lid=(0.0, 0.0, 0.0), n: int = 1) -> np.ndarray:
+    g = np.array(f, dtype=np.float64, order="C", copy=True)
+    assert g.shape[0] == q
+    _, nx, ny, nz = g.shape
+    r = lib().oracle_dqq_run(q, nx, ny, nz, int(bc), float(tau), _p(_vec3(u_lid)), int(n), _p(g))
+    if r:
+        raise MemoryError("oracle_dqq_run failed") if r == 1 else ValueError(f"unsupported lattice D3Q{q}")
+    return g
 
 
 def set_threads(n: int) -> None:

@@ -59,6 +59,15 @@ void oracle_step_box(int nx, int ny, int nz, int bc, double tau,
 void oracle_macroscopic(int nx, int ny, int nz, const double *f, double *rho,
                         double *u);
 
+/* Other cubic lattices (oracle_dqq.c): q = 15, 19 or 27, the
+ * velocity order and weights documented there.  Populations f[i][x][y][z].
+ * dqq_table: c[q][3], w[q], opp[q]; returns 1 for an unsupported q.
+ * dqq_run: n steps in place (returns 1 on allocation failure, 2 for q). */
+int oracle_dqq_table(int q, int *c, double *w, int *opp);
+void oracle_dqq_equilibrium(int q, double rho, const double u[3], double *feq);
+int oracle_dqq_collide(int q, const double *f, double omega, double *out);
+int oracle_dqq_run(int q, int nx, int ny, int nz, int bc, double tau, const double u_lid[3], long n, double *f);
+
 /* OpenMP threads used by the step loops (0 -> runtime default). */
 void oracle_set_threads(int n);
 int oracle_get_threads(void);
