@@ -177,6 +177,21 @@ typedef enum { LBM_COMM_NONE = 0, LBM_COMM_NCCL = 1, LBM_COMM_LOCAL = 2 } lbm_co
  *                   EXCHANGE. */
 typedef enum { LBM_HALO_AUTO = 0, LBM_HALO_EXCHANGE = 1, LBM_HALO_PEER = 2 } lbm_halo;
 
+/* Velocity set.  D3Q19 is the paper's and the hot path (every kernel and
+ * storage above).  D3Q15 and D3Q27 -- "no matter using D3Q15, D3Q19, D3Q27"
+ * -- run the same method (BGK with the
+ * rest-population closure, link-wise bounce-back, the moving lid, periodic
+ * wrap) as one fused collide + stream step per HBM pass on one slab
+ * (comm NONE, kernel AUTO or K1; EINVAL otherwise).  Host population arrays
+ * are f[q][nx][ny][nz] in the order lbm_lattice_table gives: i = 0 rest,
+ * 1 .. (q-1)/2 the velocities whose first nonzero component is -1 (axes,
+ * face diagonals, corners), then their opposites in the same order -- for
+ * q = 19 exactly SPEC.md:109's order. */
+typedef enum { LBM_D3Q15 = 15, LBM_D3Q19 = 19, LBM_D3Q27 = 27 } lbm_lattice;
+
+/* c[q][3] and w[q] of lattice q (15, 19, 27).  EINVAL for another q. */
+lbm_status lbm_lattice_table(int q, int *c, double *w);
+
 typedef struct {
     int struct_size;     /* sizeof(lbm_opts), for forward compatibility */
     int bc;              /* lbm_bc */
@@ -188,10 +203,11 @@ typedef struct {
     int kernel;          /* lbm_kernel */
     int local_slabs;     /* comm == LOCAL: number of slabs emulated on this device */
     int halo;            /* lbm_halo (ABI 2) */
+    int lattice;         /* lbm_lattice: 19 (default; 0 reads as 19), 15 or 27 (ABI 2) */
 } lbm_opts;
 
 /* Fills *opts with defaults: CAVITY, device -1, rank 0, world 1, NONE,
- * no id, own stream, AUTO, 1 local slab, halo AUTO. */
+ * no id, own stream, AUTO, 1 local slab, halo AUTO, D3Q19. */
 void lbm_default_opts(lbm_opts *opts);
 
 /* Create a lattice of nx*ny*nz cells with BGK relaxation time tau
@@ -233,14 +249,14 @@ lbm_status lbm_macroscopic(lbm_ctx *ctx, double *rho, double *u);
  * check: it would need a synchronisation). */
 lbm_status lbm_macroscopic_device(lbm_ctx *ctx, double *d_rho, double *d_u);
 
-/* Canonical populations f(t) as host f[19][nx_local][ny][nz] (canonical
- * direction order).  Blocks. */
+/* Canonical populations f(t) as host f[q][nx_local][ny][nz] (canonical
+ * direction order; q = 19 unless opts.lattice says otherwise).  Blocks. */
 lbm_status lbm_get_populations(lbm_ctx *ctx, double *f);
 /* The box [x0,x0+lx) x [y0,y0+ly) x [z0,z0+lz) of the slab (slab-local x)
  * as host f[19][lx][ly][lz].  EINVAL if the box leaves the slab. */
 lbm_status lbm_get_populations_box(lbm_ctx *ctx, int x0, int y0, int z0, int lx,
                                    int ly, int lz, double *f);
-/* Set the canonical state f(t) from host f[19][nx_local][ny][nz].  EINVAL if
+/* Set the canonical state f(t) from host f[q][nx_local][ny][nz].  EINVAL if
  * a value is not finite. */
 lbm_status lbm_set_populations(lbm_ctx *ctx, const double *f);
 

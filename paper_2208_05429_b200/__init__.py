@@ -31,6 +31,7 @@ LBM_KERNEL_AUTO, LBM_KERNEL_K1, LBM_KERNEL_K2, LBM_KERNEL_K2_REG, LBM_KERNEL_AA,
 LBM_KERNEL_K3 = 6
 LBM_COMM_NONE, LBM_COMM_NCCL, LBM_COMM_LOCAL = 0, 1, 2
 LBM_HALO_AUTO, LBM_HALO_EXCHANGE, LBM_HALO_PEER = 0, 1, 2
+LBM_D3Q15, LBM_D3Q19, LBM_D3Q27 = 15, 19, 27
 LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_ESTATE, LBM_ENUMERIC = 0, 1, 2, 3, 4, 5, 6
 STATUS = {0: "LBM_OK", 1: "LBM_EINVAL", 2: "LBM_ENOMEM", 3: "LBM_ECUDA", 4: "LBM_ENCCL", 5: "LBM_ESTATE",
           6: "LBM_ENUMERIC"}
@@ -47,7 +48,7 @@ class lbm_opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int), ("bc", ctypes.c_int), ("device", ctypes.c_int),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("comm", ctypes.c_int),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("kernel", ctypes.c_int),
-                ("local_slabs", ctypes.c_int), ("halo", ctypes.c_int)]
+                ("local_slabs", ctypes.c_int), ("halo", ctypes.c_int), ("lattice", ctypes.c_int)]
 
 
 class lbm_halo_plan(ctypes.Structure):
@@ -71,7 +72,7 @@ EXPORTS = ["lbm_default_opts", "lbm_create", "lbm_create_ex", "lbm_init_equilibr
            "lbm_init_equilibrium_device", "lbm_step", "lbm_macroscopic", "lbm_macroscopic_device",
            "lbm_get_populations", "lbm_get_populations_box", "lbm_set_populations", "lbm_synchronize",
            "lbm_get_time", "lbm_nccl_unique_id", "lbm_plan_halo", "lbm_profile_enable", "lbm_profile_reset",
-           "lbm_get_stats", "lbm_last_error", "lbm_destroy", "lbm_abi_version"]
+           "lbm_get_stats", "lbm_last_error", "lbm_destroy", "lbm_abi_version", "lbm_lattice_table"]
 
 
 def _load():
@@ -104,6 +105,7 @@ def _load():
         "lbm_last_error": (ctypes.c_char_p, [ctxp]),
         "lbm_destroy": (None, [ctxp]),
         "lbm_abi_version": (i, []),
+        "lbm_lattice_table": (i, [i, P(ctypes.c_int), dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -249,6 +251,14 @@ def lbm_abi_version() -> int:
     return _lib.lbm_abi_version()
 
 
+def lbm_lattice_table(q: int):
+    """(c[q,3] int, w[q] float64): the velocity order of host population arrays."""
+    c = (ctypes.c_int * (3 * q))()
+    w = np.zeros(q)
+    _check(_lib.lbm_lattice_table(int(q), c, w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    return np.array(list(c), dtype=np.int64).reshape(q, 3), w
+
+
 # --------------------------------------------------------- convenience --
 class Lattice:
     """Owner of one lbm_ctx.  Host arrays are float64 numpy arrays in the
@@ -256,9 +266,11 @@ class Lattice:
 
     def __init__(self, nx, ny, nz, tau, u_lid=(0.0, 0.0, 0.0), dtype="f64", bc=LBM_BC_CAVITY,
                  kernel=LBM_KERNEL_AUTO, comm=LBM_COMM_NONE, local_slabs=1, rank=0, world=1,
-                 nccl_id: bytes | None = None, stream=None, device=-1, halo=0):
+                 nccl_id: bytes | None = None, stream=None, device=-1, halo=0, lattice=19):
         o = lbm_default_opts()
         o.bc, o.kernel, o.comm, o.local_slabs, o.halo = bc, kernel, comm, local_slabs, halo
+        o.lattice = lattice
+        self.q = lattice
         o.rank, o.world, o.device = rank, world, device
         self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         o.nccl_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None
@@ -284,12 +296,12 @@ class Lattice:
         return rho, u
 
     def populations(self):
-        f = np.empty((19, self.nx_local, self.ny, self.nz))
+        f = np.empty((self.q, self.nx_local, self.ny, self.nz))
         lbm_get_populations(self.ctx, f)
         return f
 
     def populations_box(self, x0, y0, z0, lx, ly, lz):
-        f = np.empty((19, lx, ly, lz))
+        f = np.empty((self.q, lx, ly, lz))
         lbm_get_populations_box(self.ctx, x0, y0, z0, lx, ly, lz, f)
         return f
 

@@ -155,6 +155,12 @@ struct lbm_ctx {
     peer::Alloc pmine[2], pflags;
     peer::Alloc pnb[2][3];
     unsigned peer_seq = 0;
+    // D3Q15 / D3Q27 (dqq.cu; lbm_opts.lattice): canonical [q][nx][ny][nzp]
+    // ping-pong buffers, one fused collide + push step per launch
+    int q = 19;
+    DqqGeom dg{};
+    void* dbuf[2] = {nullptr, nullptr};
+    int dcur = 0;
     size_t esize = 8;
     int* d_flag = nullptr;
     // diagnostics
@@ -1360,6 +1366,134 @@ lbm_status get_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, d
     return wait_stream(c, c->stream);
 }
 
+// ------------------------------------------------ D3Q15 / D3Q27 (dqq.cu) --
+// Host paths of the other lattices: canonical buffers, so host arrays move
+// through the idle buffer as staging (>= 60 B per cell, enough for rho + u:
+// 32 B; populations go in x chunks).
+template <typename T>
+lbm_status dqq_init(lbm_ctx* c, const double* rho, const double* u, bool host) {
+    c->initialized = false;
+    const DqqGeom& g = c->dg;
+    const long long cells = (long long)g.nx * g.ny * g.nz;
+    T* A = static_cast<T*>(c->dbuf[c->dcur]);
+    const double* dr = rho;
+    const double* du = u;
+    if (host) {
+        double* stage = static_cast<double*>(c->dbuf[c->dcur ^ 1]);
+        dr = du = nullptr;
+        int flag = 0;
+        lbm_status st;
+        if (rho) {
+            CK(cudaMemcpyAsync(stage, rho, cells * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            dr = stage;
+            if ((st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
+            if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+        }
+        if (u) {
+            CK(cudaMemcpyAsync(stage + cells, u, 3 * cells * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            du = stage + cells;
+            if ((st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
+            if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+        }
+    }
+    CK(launch_dqq_init<T>(dr, du, A, g, c->stream));
+    c->launches++;
+    c->initialized = true;
+    c->t = 0;
+    return LBM_OK;
+}
+
+template <typename T>
+lbm_status dqq_set(lbm_ctx* c, const double* f) {
+    c->initialized = false;
+    const DqqGeom& g = c->dg;
+    const long long plane = (long long)g.ny * g.nz, cells = (long long)g.nx * plane;
+    const size_t stage_bytes = size_t(g.q) * size_t(g.pq) * c->esize;
+    const int cap = int(std::max<long long>(1, (long long)(stage_bytes / (size_t(g.q) * plane * sizeof(double)))));
+    double* stage = static_cast<double*>(c->dbuf[c->dcur ^ 1]);
+    for (int xb = 0; xb < g.nx; xb += cap) {
+        const int nxc = std::min(cap, g.nx - xb);
+        const long long cc = (long long)nxc * plane;
+        CK(cudaMemcpy2DAsync(stage, cc * sizeof(double), f + (long long)xb * plane, cells * sizeof(double),
+                             cc * sizeof(double), g.q, cudaMemcpyHostToDevice, c->stream));
+        int flag = 0;
+        lbm_status st = validate_device(c, stage, g.q * cc, false, &flag);
+        if (st != LBM_OK) return st;
+        if (flag) return fail(c, LBM_EINVAL, "populations must be finite (state is now undefined)");
+        CK(launch_dqq_import<T>(stage, static_cast<T*>(c->dbuf[c->dcur]), g, xb, nxc, c->stream));
+        c->launches++;
+    }
+    c->initialized = true;
+    c->t = 0;
+    return LBM_OK;
+}
+
+template <typename T>
+lbm_status dqq_step(lbm_ctx* c, long n) {
+    const T omega = T(1.0 / c->tau);
+    for (; n > 0; --n) {
+        size_t slot = 0;
+        lbm_status st = prof_begin(c, slot);
+        if (st != LBM_OK) return st;
+        CK(launch_dqq_step<T>(static_cast<const T*>(c->dbuf[c->dcur]), static_cast<T*>(c->dbuf[c->dcur ^ 1]), c->dg,
+                              omega, c->ulid, c->stream));
+        c->launches++;
+        c->k1_launches++;
+        if ((st = prof_end(c, slot, (long long)c->dg.nx * c->dg.ny * c->dg.nz)) != LBM_OK) return st;
+        c->dcur ^= 1;
+        c->t += 1;
+    }
+    return LBM_OK;
+}
+
+template <typename T>
+lbm_status dqq_macro(lbm_ctx* c, double* rho, double* u, bool host) {
+    const DqqGeom& g = c->dg;
+    const T* A = static_cast<const T*>(c->dbuf[c->dcur]);
+    if (!host) {
+        CK(launch_dqq_moments<T>(A, g, 0, g.nx, rho, u, nullptr, c->stream));
+        c->launches++;
+        return LBM_OK;
+    }
+    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    const long long plane = (long long)g.ny * g.nz;
+    const size_t stage_bytes = size_t(g.q) * size_t(g.pq) * c->esize;
+    const int cap = int(std::max<long long>(1, (long long)(stage_bytes / (4 * sizeof(double))) / plane));
+    double* stage = static_cast<double*>(c->dbuf[c->dcur ^ 1]);
+    for (int xb = 0; xb < g.nx; xb += cap) {
+        const int nxc = std::min(cap, g.nx - xb);
+        const long long cc = (long long)nxc * plane;
+        CK(launch_dqq_moments<T>(A, g, xb, nxc, rho ? stage : nullptr, u ? stage + cc : nullptr, c->d_flag,
+                                 c->stream));
+        c->launches++;
+        if (rho)
+            CK(cudaMemcpyAsync(rho + (long long)xb * plane, stage, cc * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
+        if (u)
+            CK(cudaMemcpyAsync(u + 3 * (long long)xb * plane, stage + cc, 3 * cc * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+    }
+    return moments_status(c);
+}
+
+template <typename T>
+lbm_status dqq_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, double* out) {
+    const DqqGeom& g = c->dg;
+    const long long bplane = (long long)ly * lz, bcells = (long long)lx * bplane;
+    const size_t stage_bytes = size_t(g.q) * size_t(g.pq) * c->esize;
+    const int cap = int(std::max<long long>(1, (long long)(stage_bytes / (size_t(g.q) * bplane * sizeof(double)))));
+    double* stage = static_cast<double*>(c->dbuf[c->dcur ^ 1]);
+    for (int xb = bx; xb < bx + lx; xb += cap) {
+        const int nxc = std::min(cap, bx + lx - xb);
+        const long long cc = (long long)nxc * bplane;
+        CK(launch_dqq_box<T>(static_cast<const T*>(c->dbuf[c->dcur]), g, xb, by, bz, nxc, ly, lz, stage, c->stream));
+        c->launches++;
+        CK(cudaMemcpy2DAsync(out + (long long)(xb - bx) * bplane, bcells * sizeof(double), stage,
+                             cc * sizeof(double), cc * sizeof(double), g.q, cudaMemcpyDeviceToHost, c->stream));
+    }
+    return wait_stream(c, c->stream);
+}
+
 // LBM_HALO_PEER set-up (after the lattice buffers exist): a flag page,
 // then every rank hands its buffers and flag page to its neighbours as file
 // descriptors over the rendezvous socket and maps theirs (peer.cu).
@@ -1430,6 +1564,24 @@ void lbm_default_opts(lbm_opts* o) {
     o->kernel = LBM_KERNEL_AUTO;
     o->local_slabs = 1;
     o->halo = LBM_HALO_AUTO;
+    o->lattice = 19;
+}
+
+lbm_status lbm_lattice_table(int q, int* c, double* w) {
+    lbm_ctx* ctx = nullptr;
+    if (!c || !w) return fail(ctx, LBM_EINVAL, "null argument");
+    if (q == 19) {
+        for (int i = 0; i < 19; ++i) {
+            c[3 * i] = can_cx(i);
+            c[3 * i + 1] = can_cy(i);
+            c[3 * i + 2] = can_cz(i);
+            w[i] = i == 0 ? 1.0 / 3.0 : (can_axis(i) ? 1.0 / 18.0 : 1.0 / 36.0);
+        }
+        return LBM_OK;
+    }
+    if (q != 15 && q != 27) return fail(ctx, LBM_EINVAL, "bad lattice %d (15, 19 or 27)", q);
+    dqq_table(q, c, w);
+    return LBM_OK;
 }
 
 const char* lbm_last_error(const lbm_ctx* c) { return c ? c->err.c_str() : t_last_error.c_str(); }
@@ -1489,6 +1641,11 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         (dt != LBM_F32 || o.bc != LBM_BC_PERIODIC || o.comm != LBM_COMM_NONE))
         return fail(c, LBM_EINVAL, "kernel K3 (three-step prototype) needs fp32, a periodic box and comm NONE");
     if (o.halo < LBM_HALO_AUTO || o.halo > LBM_HALO_PEER) return fail(c, LBM_EINVAL, "bad halo %d", o.halo);
+    const int q = o.lattice == 0 ? 19 : o.lattice;
+    if (q != 15 && q != 19 && q != 27) return fail(c, LBM_EINVAL, "bad lattice %d (15, 19 or 27)", o.lattice);
+    if (q != 19 && (o.comm != LBM_COMM_NONE || o.halo != LBM_HALO_AUTO ||
+                    (o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K1)))
+        return fail(c, LBM_EINVAL, "lattice D3Q%d: one slab (comm NONE), kernel AUTO or K1", q);
     if (o.halo == LBM_HALO_PEER && o.comm != LBM_COMM_NCCL)
         return fail(c, LBM_EINVAL, "halo PEER needs comm NCCL (world 1: the periodic self-wrap)");
     if (o.halo == LBM_HALO_PEER && o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K2)
@@ -1575,6 +1732,27 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         for (cudaEvent_t& ev : c->progress)
             if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
                 return bail(fail(c, LBM_ECUDA, "progress events"));
+    }
+    if (q != 19) {  // D3Q15 / D3Q27: two canonical buffers, nothing else
+        c->q = q;
+        c->dg.q = q;
+        c->dg.nx = nx;
+        c->dg.ny = ny;
+        c->dg.nz = nz;
+        c->dg.nzp = round_up(nz, int(32 / c->esize));
+        c->dg.bc = o.bc;
+        c->dg.pq = (long long)nx * ny * c->dg.nzp;
+        const size_t bytes = size_t(q) * size_t(c->dg.pq) * c->esize;
+        for (int b = 0; b < 2; ++b) {
+            if (cudaMalloc(&c->dbuf[b], bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return bail(fail(c, LBM_ENOMEM, "cudaMalloc(%zu bytes)", bytes));
+            }
+            if (cudaMemset(c->dbuf[b], 0, bytes) != cudaSuccess) return bail(fail(c, LBM_ECUDA, "cudaMemset"));
+        }
+        if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(c, LBM_ECUDA, "create sync"));
+        *out = c;
+        return LBM_OK;
     }
     // AUTO: two lattice copies (K2) unless they do not fit the device's free
     // memory while the single-copy ring does -- then K2_SC (the paper's point
@@ -1726,6 +1904,8 @@ void lbm_destroy(lbm_ctx* c) {
     for (Slab& s : c->slabs)
         for (void* b : s.buf)
             if (b) cudaFree(b);
+    for (void* b : c->dbuf)
+        if (b) cudaFree(b);
     if (c->d_flag) cudaFree(c->d_flag);
     if (c->sc_sync) cudaFree(c->sc_sync);
     if (c->stage) cudaFree(c->stage);
@@ -1749,6 +1929,7 @@ lbm_status lbm_init_equilibrium(lbm_ctx* c, const double* rho, const double* u) 
     DeviceGuard dg;
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
+    if (c->q != 19) return c->dt == LBM_F64 ? dqq_init<double>(c, rho, u, true) : dqq_init<float>(c, rho, u, true);
     return c->dt == LBM_F64 ? init_eq<double>(c, rho, u, true) : init_eq<float>(c, rho, u, true);
 }
 
@@ -1756,6 +1937,7 @@ lbm_status lbm_init_equilibrium_device(lbm_ctx* c, const double* rho, const doub
     DeviceGuard dg;
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
+    if (c->q != 19) return c->dt == LBM_F64 ? dqq_init<double>(c, rho, u, false) : dqq_init<float>(c, rho, u, false);
     return c->dt == LBM_F64 ? init_eq<double>(c, rho, u, false) : init_eq<float>(c, rho, u, false);
 }
 
@@ -1764,6 +1946,7 @@ lbm_status lbm_set_populations(lbm_ctx* c, const double* f) {
     lbm_status st = entry(c, false);
     if (st != LBM_OK) return st;
     if (!f) return fail(c, LBM_EINVAL, "f is NULL");
+    if (c->q != 19) return c->dt == LBM_F64 ? dqq_set<double>(c, f) : dqq_set<float>(c, f);
     return c->dt == LBM_F64 ? set_pops<double>(c, f) : set_pops<float>(c, f);
 }
 
@@ -1772,6 +1955,7 @@ lbm_status lbm_step(lbm_ctx* c, long n) {
     if (c && n < 0) return fail(c, LBM_EINVAL, "n must be >= 0 (got %ld)", n);
     lbm_status st = entry(c, true);
     if (st != LBM_OK) return st;
+    if (c->q != 19) return c->dt == LBM_F64 ? dqq_step<double>(c, n) : dqq_step<float>(c, n);
     return c->dt == LBM_F64 ? run_steps<double>(c, n) : run_steps<float>(c, n);
 }
 
@@ -1779,6 +1963,7 @@ lbm_status lbm_macroscopic(lbm_ctx* c, double* rho, double* u) {
     DeviceGuard dg;
     lbm_status st = entry(c, true);
     if (st != LBM_OK) return st;
+    if (c->q != 19) return c->dt == LBM_F64 ? dqq_macro<double>(c, rho, u, true) : dqq_macro<float>(c, rho, u, true);
     return c->dt == LBM_F64 ? macro<double>(c, rho, u, true) : macro<float>(c, rho, u, true);
 }
 
@@ -1786,6 +1971,7 @@ lbm_status lbm_macroscopic_device(lbm_ctx* c, double* rho, double* u) {
     DeviceGuard dg;
     lbm_status st = entry(c, true);
     if (st != LBM_OK) return st;
+    if (c->q != 19) return c->dt == LBM_F64 ? dqq_macro<double>(c, rho, u, false) : dqq_macro<float>(c, rho, u, false);
     return c->dt == LBM_F64 ? macro<double>(c, rho, u, false) : macro<float>(c, rho, u, false);
 }
 
@@ -1797,6 +1983,10 @@ lbm_status lbm_get_populations_box(lbm_ctx* c, int x0, int y0, int z0, int lx, i
     if (lx < 0 || ly < 0 || lz < 0 || x0 < 0 || y0 < 0 || z0 < 0 || x0 + lx > c->nxl_proc || y0 + ly > c->ny ||
         z0 + lz > c->nz)
         return fail(c, LBM_EINVAL, "box outside the slab");
+    if (c->q != 19)
+        return (long long)lx * ly * lz == 0 ? LBM_OK
+               : c->dt == LBM_F64           ? dqq_box<double>(c, x0, y0, z0, lx, ly, lz, f)
+                                            : dqq_box<float>(c, x0, y0, z0, lx, ly, lz, f);
     if ((long long)lx * ly * lz == 0) return ensure_ghosts(c);  // collective under NCCL: every rank exchanges
     return c->dt == LBM_F64 ? get_box<double>(c, x0, y0, z0, lx, ly, lz, f)
                             : get_box<float>(c, x0, y0, z0, lx, ly, lz, f);

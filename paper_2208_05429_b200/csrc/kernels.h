@@ -54,6 +54,26 @@ bool k3_supported(const SlabGeom& g);
 template <typename T>
 cudaError_t launch_k3(const T* A, T* B, const StepParams<T>& P, cudaStream_t s);
 
+// D3Q15 / D3Q27 (dqq.cu): canonical storage [q][nx][ny][nzp], one fused
+// collide + push step per launch; a single slab, no ghost planes.
+struct DqqGeom {
+    int q, nx, ny, nz, nzp, bc;
+    long long pq;  // elements per direction = nx * ny * nzp
+};
+template <typename T>
+cudaError_t launch_dqq_step(const T* A, T* B, const DqqGeom& g, T omega, const double ulid[3], cudaStream_t s);
+template <typename T>
+cudaError_t launch_dqq_init(const double* rho, const double* u, T* A, const DqqGeom& g, cudaStream_t s);
+template <typename T>
+cudaError_t launch_dqq_moments(const T* A, const DqqGeom& g, int xbeg, int nxc, double* rho, double* u, int* flag,
+                               cudaStream_t s);
+template <typename T>
+cudaError_t launch_dqq_box(const T* A, const DqqGeom& g, int x0, int y0, int z0, int lx, int ly, int lz, double* out,
+                           cudaStream_t s);
+template <typename T>
+cudaError_t launch_dqq_import(const double* src, T* A, const DqqGeom& g, int xbeg, int nxc, cudaStream_t s);
+void dqq_table(int q, int* c, double* w);
+
 // canonical feq of planes [xbeg, xbeg + nxc) (nxc < 0: the whole slab); rho/u
 // point at the first of those planes
 template <typename T>

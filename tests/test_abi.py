@@ -112,6 +112,33 @@ def test_k3_rejects_unsupported():
         lbm.lbm_create_ex(16, 8, 32, 0.6, None, "f32", o)
 
 
+@pytest.mark.parametrize("q", [15, 19, 27])
+def test_lattice_table_matches_oracle_convention(q):
+    """The host direction order of lbm_lattice_table is the oracle's
+    (oracle_dqq.c; D3Q19: SPEC.md:109) -- same velocities, same weights."""
+    import oracle
+    c, w = lbm.lbm_lattice_table(q)
+    c0, w0, _ = oracle.dqq_table(q)
+    assert np.array_equal(c, c0) and np.array_equal(w, w0)
+
+
+def test_lattice_validation():
+    o = lbm.lbm_default_opts()
+    assert o.lattice == 19
+    o.lattice = 21
+    with pytest.raises(lbm.LbmError, match="bad lattice"):
+        lbm.lbm_create_ex(8, 8, 8, 0.6, None, "f64", o)
+    o.lattice, o.comm, o.local_slabs = 27, lbm.LBM_COMM_LOCAL, 2
+    with pytest.raises(lbm.LbmError, match="D3Q27"):
+        lbm.lbm_create_ex(8, 8, 8, 0.6, None, "f64", o)
+    o = lbm.lbm_default_opts()
+    o.lattice, o.kernel = 15, lbm.LBM_KERNEL_K2
+    with pytest.raises(lbm.LbmError, match="D3Q15"):
+        lbm.lbm_create_ex(8, 8, 8, 0.6, None, "f64", o)
+    with pytest.raises(lbm.LbmError):
+        lbm.lbm_lattice_table(21)
+
+
 def test_header_enums_match_binding():
     """Every enumerator of include/lbm.h has the same value in the binding."""
     src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "lbm.h")).read(), flags=re.S)

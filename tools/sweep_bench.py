@@ -26,13 +26,14 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tag", default="")
 ap.add_argument("--slabs", type=int, default=1, help="LOCAL X-slabs on this GPU (exchange path)")
 ap.add_argument("--power", action="store_true", help="also sample SM clock and board power (NVML)")
+ap.add_argument("--lattice", type=int, default=19, help="19, or 15 / 27 (one-step kernel)")
 a = ap.parse_args()
 nx, ny, nz = (int(v) for v in a.dims.split(","))
 kern = {"auto": 0, "k1": 1, "k2": 2, "aa": 4, "k2sc": 5, "k3": 6}[a.kernel]
 bc = lbm.LBM_BC_CAVITY if a.bc == "cavity" else lbm.LBM_BC_PERIODIC
 es = 8 if a.dtype == "f64" else 4
 kw = dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=a.slabs) if a.slabs > 1 else {}
-with lbm.Lattice(nx, ny, nz, 0.6, (0.05, 0, 0), a.dtype, bc=bc, kernel=kern, **kw) as lat:
+with lbm.Lattice(nx, ny, nz, 0.6, (0.05, 0, 0), a.dtype, bc=bc, kernel=kern, lattice=a.lattice, **kw) as lat:
     lat.init_equilibrium(None, None)
     lat.step(4)
     lbm.lbm_synchronize(lat.ctx)
@@ -74,7 +75,7 @@ with lbm.Lattice(nx, ny, nz, 0.6, (0.05, 0, 0), a.dtype, bc=bc, kernel=kern, **k
         pw = statistics.median(x[1] for x in tail)
     best = max(r[0] for r in res)
     med = statistics.median(r[0] for r in res)
-    gbs = best * 1e6 * 19 * es * (2 / steps_per) / 1e9
+    gbs = best * 1e6 * a.lattice * es * (2 / steps_per) / 1e9
     print(f"{a.tag or a.kernel:24s} {a.dtype} {a.dims:14s} best {best:9.1f} MLUPS  median {med:9.1f}  "
           f"sweep {min(r[1] for r in res):8.3f} ms  algorithmic {gbs:7.1f} GB/s  "
           f"whole-step {max(r[2] for r in res):9.1f} MLUPS"
