@@ -150,6 +150,18 @@ typedef enum {
     LBM_KERNEL_K3 = 6
 } lbm_kernel;
 
+/* X-Y partition (the paper's future work "partition a
+ * 3D domain along three axes"), emulated on one device like
+ * the LOCAL X-slabs: opts.local_blocks_y > 1 splits each of the
+ * local_slabs x ranges into that many y blocks (ny divisible, >= 4 rows
+ * each).  Every block carries 2 frame rows per side holding its
+ * y-neighbours' edge rows; before a sweep the frame rows are exchanged
+ * (block to block), then the x ghost planes (which carry them along, so the
+ * x-y edge cells come from the diagonal block).  Cavity walls only at the
+ * domain's ends; a periodic box wraps around the blocks.  Two-buffer K1/K2
+ * storage (kernel AUTO, K1 or K2), D3Q19; EINVAL otherwise.  Host arrays
+ * cover the whole domain as usual.  Bitwise identical to one slab. */
+
 /* Halo transport between X-slabs (PAPER.md:336 X-only partition).
  *  NONE   world == 1 and local_slabs == 1 (periodic x wraps onto itself)
  *  NCCL   one slab per process/GPU, ncclSend/ncclRecv over NVLink
@@ -204,6 +216,8 @@ typedef struct {
     int local_slabs;     /* comm == LOCAL: number of slabs emulated on this device */
     int halo;            /* lbm_halo (ABI 2) */
     int lattice;         /* lbm_lattice: 19 (default; 0 reads as 19), 15 or 27 (ABI 2) */
+    int local_blocks_y;  /* comm == LOCAL: also split every x slab into this many y blocks
+                            (X-Y partition; 0 or 1 = none) (ABI 2) */
 } lbm_opts;
 
 /* Fills *opts with defaults: CAVITY, device -1, rank 0, world 1, NONE,

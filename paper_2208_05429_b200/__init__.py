@@ -48,7 +48,8 @@ class lbm_opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int), ("bc", ctypes.c_int), ("device", ctypes.c_int),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("comm", ctypes.c_int),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("kernel", ctypes.c_int),
-                ("local_slabs", ctypes.c_int), ("halo", ctypes.c_int), ("lattice", ctypes.c_int)]
+                ("local_slabs", ctypes.c_int), ("halo", ctypes.c_int), ("lattice", ctypes.c_int),
+                ("local_blocks_y", ctypes.c_int)]
 
 
 class lbm_halo_plan(ctypes.Structure):
@@ -266,10 +267,11 @@ class Lattice:
 
     def __init__(self, nx, ny, nz, tau, u_lid=(0.0, 0.0, 0.0), dtype="f64", bc=LBM_BC_CAVITY,
                  kernel=LBM_KERNEL_AUTO, comm=LBM_COMM_NONE, local_slabs=1, rank=0, world=1,
-                 nccl_id: bytes | None = None, stream=None, device=-1, halo=0, lattice=19):
+                 nccl_id: bytes | None = None, stream=None, device=-1, halo=0, lattice=19, local_blocks_y=1):
         o = lbm_default_opts()
         o.bc, o.kernel, o.comm, o.local_slabs, o.halo = bc, kernel, comm, local_slabs, halo
         o.lattice = lattice
+        o.local_blocks_y = local_blocks_y
         self.q = lattice
         o.rank, o.world, o.device = rank, world, device
         self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None

@@ -102,6 +102,8 @@ struct Slab {
     SlabGeom g;
     void* buf[2] = {nullptr, nullptr};
     int left = -1, right = -1;  // neighbour slab index (LOCAL/NONE) or rank (NCCL); -1 = wall
+    int down = -1, up = -1;     // X-Y blocks: neighbour slab index in -y / +y; -1 = wall or none
+    int y0 = 0;                 // X-Y blocks: first global row of this slab
     lbm_halo_plan plan;
 };
 
@@ -118,6 +120,7 @@ struct lbm_ctx {
     // periodic ghost frame (SlabGeom) of the state buffer's own planes is
     // current: K2 sweeps keep it, every other writer clears it
     bool frame_valid = false;
+    int yblocks = 1;  // X-Y blocks (LOCAL, local_blocks_y): slabs per x range, split along y
     long t = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -320,8 +323,11 @@ lbm_status peer_signal(lbm_ctx* c) {
 
 // ghost_rows: periodic frame rows per side -- 2 (K2's reach), 3 for the
 // three-step K3 (a K3 context's own plan; lbm_plan_halo describes K2's)
+// yframe: an X-Y block -- ny is the block's own row count and the plane has
+// 2 frame rows per side for the y-neighbours' rows (both boundary modes; the
+// z frame columns stay periodic-only)
 void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world, int nxl, int x0,
-               lbm_halo_plan* p, int ghost_rows = 2) {
+               lbm_halo_plan* p, int ghost_rows = 2, bool yframe = false) {
     memset(p, 0, sizeof *p);
     p->nx_local = nxl;
     p->x0 = x0;
@@ -336,7 +342,7 @@ void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world
         p->z_offset = sector;
         p->nz_pitch = round_up(sector + nz + sector, sector);
     } else {
-        p->y_ghost = 0;
+        p->y_ghost = yframe ? 2 : 0;
         p->z_offset = 0;
         p->nz_pitch = round_up(nz, sector);
     }
@@ -470,6 +476,30 @@ lbm_status exchange(lbm_ctx* c, int which, cudaStream_t st) {
         if (s.left >= 0) CKN(g_nccl.Recv(b + s.plan.recv_left_off * es, n, ty, s.left, c->comm, st));
         CKN(g_nccl.GroupEnd());
     } else {
+        // X-Y blocks: first the frame rows of every block's own planes from
+        // its y-neighbours (2 rows x whole pitch per (plane, slot): one
+        // strided copy per side), then the x ghost planes below, which carry
+        // those rows along -- so the x-y edge entries come from the diagonal
+        // block
+        if (c->yblocks > 1) {
+            const size_t es = c->esize;
+            for (Slab& s : c->slabs) {
+                const long long gyz = (long long)s.g.gy * s.g.nzp;  // one frame band
+                const size_t width = size_t(gyz) * es, pitch = size_t(s.g.pq) * es;
+                char* mine = static_cast<char*>(s.buf[which]) + 2 * s.g.px * (long long)es;
+                if (s.down >= 0) {  // my rows [-gy, 0) <- its rows [ny - gy, ny)
+                    const Slab& D = c->slabs[s.down];
+                    const char* src = static_cast<const char*>(D.buf[which]) + (2 * D.g.px + (long long)D.g.ny * D.g.nzp) * (long long)es;
+                    CK(cudaMemcpy2DAsync(mine, pitch, src, pitch, width, size_t(s.g.nxl) * kQ, cudaMemcpyDeviceToDevice, st));
+                }
+                if (s.up >= 0) {  // my rows [ny, ny + gy) <- its rows [0, gy)
+                    const Slab& U = c->slabs[s.up];
+                    const char* src = static_cast<const char*>(U.buf[which]) + (2 * U.g.px + gyz) * (long long)es;
+                    CK(cudaMemcpy2DAsync(mine + (gyz + (long long)s.g.ny * s.g.nzp) * (long long)es, pitch, src, pitch,
+                                         width, size_t(s.g.nxl) * kQ, cudaMemcpyDeviceToDevice, st));
+                }
+            }
+        }
         for (Slab& s : c->slabs) {
             char* dst = static_cast<char*>(s.buf[which]);
             const size_t bytes = size_t(s.plan.span) * c->esize;
@@ -573,7 +603,7 @@ bool aa_has_halo(const lbm_ctx* c) {
 
 bool has_neighbours(const lbm_ctx* c) {
     for (const Slab& s : c->slabs)
-        if (s.left >= 0 || s.right >= 0) return true;
+        if (s.left >= 0 || s.right >= 0 || s.down >= 0 || s.up >= 0) return true;
     return false;
 }
 
@@ -792,7 +822,7 @@ lbm_status run_steps(lbm_ctx* c, long n) {
     // no exchange runs.  LBM_FUSED_HALO=0 turns it off (A/B runs, tests).
     // With NCCL ranks the same stores go into the neighbours' buffers as
     // mapped here (LBM_HALO_PEER, peer.cu).
-    const bool fuse = tma && c->fused_halo && (c->opts.comm != LBM_COMM_NCCL || c->peer);
+    const bool fuse = tma && c->fused_halo && (c->opts.comm != LBM_COMM_NCCL || c->peer) && c->yblocks == 1;
     while (n > 0) {
         const int nsteps = (use_k2 && n >= 2) ? 2 : 1;
         const bool fused = fuse && nsteps == 2;
@@ -826,7 +856,7 @@ lbm_status run_steps(lbm_ctx* c, long n) {
             if (fst != LBM_OK) return fst;
         }
         const int h = nsteps;
-        bool split = !c->ghosts_valid && has_neighbours(c) && c->overlap;
+        bool split = !c->ghosts_valid && has_neighbours(c) && c->overlap && c->yblocks == 1;
         for (const Slab& s : c->slabs) split = split && s.g.nxl >= 2 * h + 2;
         if (!c->ghosts_valid && has_neighbours(c) && !split) {
             lbm_status st = exchange(c, c->cur, c->stream);
@@ -1143,6 +1173,148 @@ lbm_status set_pops_sc(lbm_ctx* c, const double* f) {
     return sc_init_done(c);
 }
 
+// ------------------------------------------------------- X-Y blocks ----
+lbm_status moments_status(lbm_ctx* c);
+// Host / device arrays cover the whole domain; a block's part of one is a
+// 3D sub-box: planes [x, x + nxc) of rows [y0, y0 + ny) of k doubles per
+// cell.  Copy it to / from a contiguous [nxc][ny][nz * k] array.
+lbm_status copy_block(lbm_ctx* c, double* dst, const double* src, bool to_block, const Slab& s, int xb, int nxc,
+                      int k, cudaMemcpyKind kind) {
+    cudaMemcpy3DParms m;
+    memset(&m, 0, sizeof m);
+    const size_t row = size_t(c->nz) * size_t(k) * sizeof(double);
+    const cudaPos gpos = make_cudaPos(0, size_t(s.y0), size_t(s.g.x0 - c->x0_proc + xb));
+    if (to_block) {
+        m.srcPtr = make_cudaPitchedPtr(const_cast<double*>(src), row, row, size_t(c->ny));
+        m.srcPos = gpos;
+        m.dstPtr = make_cudaPitchedPtr(dst, row, row, size_t(s.g.ny));
+    } else {
+        m.srcPtr = make_cudaPitchedPtr(const_cast<double*>(src), row, row, size_t(s.g.ny));
+        m.dstPtr = make_cudaPitchedPtr(dst, row, row, size_t(c->ny));
+        m.dstPos = gpos;
+    }
+    m.extent = make_cudaExtent(row, size_t(s.g.ny), size_t(nxc));
+    m.kind = kind;
+    CK(cudaMemcpy3DAsync(&m, c->stream));
+    return LBM_OK;
+}
+
+template <typename T>
+lbm_status init_eq_blocks(lbm_ctx* c, const double* rho, const double* u, bool host) {
+    const int canon = c->cur;
+    const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    for (Slab& s : c->slabs) {
+        const long long cells = (long long)s.g.nxl * s.g.ny * s.g.nz;
+        double* stage = static_cast<double*>(s.buf[canon ^ 1]);  // >= 32 B per cell
+        const double* dr = nullptr;
+        const double* du = nullptr;
+        lbm_status st;
+        if (rho) {
+            if ((st = copy_block(c, stage, rho, true, s, 0, s.g.nxl, 1, kind)) != LBM_OK) return st;
+            dr = stage;
+        }
+        if (u) {
+            if ((st = copy_block(c, stage + cells, u, true, s, 0, s.g.nxl, 3, kind)) != LBM_OK) return st;
+            du = stage + cells;
+        }
+        if (host) {
+            int flag = 0;
+            if (dr && (st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
+            if (flag) return agree_valid(c, 1, "rho must be finite and > 0");
+            if (du && (st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
+            if (flag) return agree_valid(c, 1, "u must be finite");
+        }
+        CK(launch_k0_equilibrium<T>(dr, du, origin<T>(s, canon), s.g, c->stream));
+        c->launches++;
+    }
+    return finish_init<T>(c, canon);
+}
+
+template <typename T>
+lbm_status set_pops_blocks(lbm_ctx* c, const double* f) {
+    const int canon = c->cur ^ 1;
+    const long long proc_cells = (long long)c->nxl_proc * c->ny * c->nz;
+    c->initialized = false;
+    for (Slab& s : c->slabs) {
+        const long long plane = (long long)s.g.ny * s.g.nz;
+        double* stage = static_cast<double*>(s.buf[canon ^ 1]);
+        const long long cap = std::max<long long>(
+            1, (long long)(size_t(s.plan.buffer_elems) * c->esize) / (kQ * plane * (long long)sizeof(double)));
+        for (int xb = 0; xb < s.g.nxl; xb += int(cap)) {
+            const int nxc = int(std::min<long long>(cap, s.g.nxl - xb));
+            const long long cc = (long long)nxc * plane;
+            for (int i = 0; i < kQ; ++i) {
+                lbm_status st = copy_block(c, stage + i * cc, f + i * proc_cells, true, s, xb, nxc, 1,
+                                           cudaMemcpyHostToDevice);
+                if (st != LBM_OK) return st;
+            }
+            int flag = 0;
+            lbm_status st = validate_device(c, stage, kQ * cc, false, &flag);
+            if (st != LBM_OK) return st;
+            if (flag) return agree_valid(c, 1, "populations must be finite");
+            CK(launch_k0_import<T>(stage, origin<T>(s, canon), s.g, xb, nxc, c->stream));
+            c->launches++;
+        }
+    }
+    return finish_init<T>(c, canon);
+}
+
+template <typename T>
+lbm_status macro_blocks(lbm_ctx* c, double* rho, double* u, bool host) {
+    lbm_status st = ensure_ghosts(c);
+    if (st != LBM_OK) return st;
+    int* const flag = host ? c->d_flag : nullptr;
+    if (flag) CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+    const cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    for (Slab& s : c->slabs) {
+        const long long cells = (long long)s.g.nxl * s.g.ny * s.g.nz;
+        double* stage = static_cast<double*>(s.buf[c->cur ^ 1]);
+        CK(launch_k3_moments<T>(origin<T>(s, c->cur), make_params<T>(c, s), 0, s.g.nxl, rho ? stage : nullptr,
+                                u ? stage + cells : nullptr, c->stream, flag));
+        c->launches++;
+        if (rho && (st = copy_block(c, rho, stage, false, s, 0, s.g.nxl, 1, kind)) != LBM_OK) return st;
+        if (u && (st = copy_block(c, u, stage + cells, false, s, 0, s.g.nxl, 3, kind)) != LBM_OK) return st;
+    }
+    return host ? moments_status(c) : LBM_OK;
+}
+
+template <typename T>
+lbm_status get_box_blocks(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, double* out) {
+    lbm_status st = ensure_ghosts(c);
+    if (st != LBM_OK) return st;
+    const long long bcells = (long long)lx * ly * lz;
+    for (Slab& s : c->slabs) {
+        const int sx0 = s.g.x0 - c->x0_proc;
+        const int xa = std::max(bx, sx0), xb = std::min(bx + lx, sx0 + s.g.nxl);
+        const int ya = std::max(by, s.y0), yb = std::min(by + ly, s.y0 + s.g.ny);
+        if (xa >= xb || ya >= yb) continue;
+        const int nyc = yb - ya;
+        double* stage = static_cast<double*>(s.buf[c->cur ^ 1]);
+        // x chunks that fit the staging buffer (the slab's idle lattice buffer)
+        const long long cap = std::max<long long>(
+            1, (long long)(size_t(s.plan.buffer_elems) * c->esize) / (kQ * (long long)nyc * lz * (long long)sizeof(double)));
+        for (int x = xa; x < xb; x += int(cap)) {
+            const int nxc = int(std::min<long long>(cap, xb - x));
+            const long long cc = (long long)nxc * nyc * lz;
+            CK(launch_k3_materialize<T>(origin<T>(s, c->cur), make_params<T>(c, s), x - sx0, ya - s.y0, bz, nxc, nyc,
+                                        lz, stage, c->stream));
+            c->launches++;
+            for (int i = 0; i < kQ; ++i) {
+                cudaMemcpy3DParms m;
+                memset(&m, 0, sizeof m);
+                const size_t row = size_t(lz) * sizeof(double);
+                m.srcPtr = make_cudaPitchedPtr(stage + i * cc, row, row, size_t(nyc));
+                m.dstPtr = make_cudaPitchedPtr(out + i * bcells, row, row, size_t(ly));
+                m.dstPos = make_cudaPos(0, size_t(ya - by), size_t(x - bx));
+                m.extent = make_cudaExtent(row, size_t(nyc), size_t(nxc));
+                m.kind = cudaMemcpyDeviceToHost;
+                CK(cudaMemcpy3DAsync(&m, c->stream));
+            }
+        }
+    }
+    return wait_stream(c, c->stream);
+}
+
 template <typename T>
 lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
     // peer halo: no neighbour still writes into (or reads) these buffers
@@ -1151,6 +1323,7 @@ lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
     // the state is rewritten from here on: invalid until the init completes
     // (a rejected input leaves it undefined, include/lbm.h)
     c->initialized = false;
+    if (c->yblocks > 1) return init_eq_blocks<T>(c, rho, u, host);
     if (c->aa) return init_eq_aa<T>(c, rho, u, host);
     if (c->sc) return init_eq_sc<T>(c, rho, u, host);
     const long long plane = (long long)c->ny * c->nz;
@@ -1206,6 +1379,7 @@ lbm_status set_pops(lbm_ctx* c, const double* f) {
     if (c->sc) return set_pops_sc<T>(c, f);
     lbm_status pst = peer_wait(c);  // peer halo: the neighbours are done with these buffers
     if (pst != LBM_OK) return pst;
+    if (c->yblocks > 1) return set_pops_blocks<T>(c, f);
     const long long plane = (long long)c->ny * c->nz;
     const long long proc_cells = (long long)c->nxl_proc * plane;
     // import into the non-state buffer, stage in the state buffer (AA: into
@@ -1289,6 +1463,7 @@ lbm_status macro_aa(lbm_ctx* c, double* rho, double* u, bool host) {
 template <typename T>
 lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
     if (c->aa || c->sc) return macro_aa<T>(c, rho, u, host);
+    if (c->yblocks > 1) return macro_blocks<T>(c, rho, u, host);
     lbm_status st = ensure_ghosts(c);
     if (st != LBM_OK) return st;
     int* const flag = host ? c->d_flag : nullptr;  // the blocking read-back checks the moments
@@ -1335,6 +1510,7 @@ lbm_status macro(lbm_ctx* c, double* rho, double* u, bool host) {
 // box in process-local coordinates; out f[19][lx][ly][lz]
 template <typename T>
 lbm_status get_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, double* out) {
+    if (c->yblocks > 1) return get_box_blocks<T>(c, bx, by, bz, lx, ly, lz, out);
     lbm_status st = ensure_ghosts(c);
     if (st != LBM_OK) return st;
     const long long bplane = (long long)ly * lz;
@@ -1565,6 +1741,7 @@ void lbm_default_opts(lbm_opts* o) {
     o->local_slabs = 1;
     o->halo = LBM_HALO_AUTO;
     o->lattice = 19;
+    o->local_blocks_y = 1;
 }
 
 lbm_status lbm_lattice_table(int q, int* c, double* w) {
@@ -1641,9 +1818,17 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         (dt != LBM_F32 || o.bc != LBM_BC_PERIODIC || o.comm != LBM_COMM_NONE))
         return fail(c, LBM_EINVAL, "kernel K3 (three-step prototype) needs fp32, a periodic box and comm NONE");
     if (o.halo < LBM_HALO_AUTO || o.halo > LBM_HALO_PEER) return fail(c, LBM_EINVAL, "bad halo %d", o.halo);
+    const int by = o.local_blocks_y < 1 ? 1 : o.local_blocks_y;
+    if (by > 1) {
+        if (o.comm != LBM_COMM_LOCAL)
+            return fail(c, LBM_EINVAL, "local_blocks_y > 1 (X-Y blocks) needs comm LOCAL");
+        if (ny % by || ny / by < 4) return fail(c, LBM_EINVAL, "X-Y blocks: ny %% local_blocks_y == 0, >= 4 rows each");
+        if (o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K1 && o.kernel != LBM_KERNEL_K2)
+            return fail(c, LBM_EINVAL, "X-Y blocks run the two-buffer K1/K2 storage (kernel AUTO, K1 or K2)");
+    }
     const int q = o.lattice == 0 ? 19 : o.lattice;
     if (q != 15 && q != 19 && q != 27) return fail(c, LBM_EINVAL, "bad lattice %d (15, 19 or 27)", o.lattice);
-    if (q != 19 && (o.comm != LBM_COMM_NONE || o.halo != LBM_HALO_AUTO ||
+    if (q != 19 && (o.comm != LBM_COMM_NONE || o.halo != LBM_HALO_AUTO || by > 1 ||
                     (o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K1)))
         return fail(c, LBM_EINVAL, "lattice D3Q%d: one slab (comm NONE), kernel AUTO or K1", q);
     if (o.halo == LBM_HALO_PEER && o.comm != LBM_COMM_NCCL)
@@ -1687,7 +1872,8 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     c->nxl_proc = nx / o.world;
     c->x0_proc = o.rank * c->nxl_proc;
     const int sw = o.local_slabs;
-    c->slabs.resize(sw);
+    c->yblocks = by;
+    c->slabs.resize(size_t(sw) * by);  // slab j = (x range j / by, y block j % by)
     // scratch word(s): validation flags, NCCL agreement (8 bytes)
     if (cudaMalloc(&c->d_flag, 16) != cudaSuccess) return bail(fail(c, LBM_ENOMEM, "cudaMalloc flag"));
     if (o.stream) {
@@ -1760,7 +1946,7 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     // free memory considered (tests).
     bool use_sc = o.kernel == LBM_KERNEL_K2_SC;
     c->peer = o.halo == LBM_HALO_PEER;
-    if (o.kernel == LBM_KERNEL_AUTO && !c->peer) {
+    if (o.kernel == LBM_KERNEL_AUTO && !c->peer && by == 1) {
         size_t freeb = 0, totalb = 0;
         if (cudaMemGetInfo(&freeb, &totalb) != cudaSuccess) {
             cudaGetLastError();
@@ -1791,13 +1977,25 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         const size_t margin = size_t(256) << 20;
         if (two + margin > freeb && one + margin <= freeb) use_sc = true;
     }
-    for (int j = 0; j < sw; ++j) {
+    const int nyl = ny / by;
+    for (int j = 0; j < sw * by; ++j) {
         Slab& s = c->slabs[j];
-        const int grank = o.rank * sw + j;  // global slab index
-        fill_plan(nx, ny, nz, c->esize, o.bc, grank, nslab_total, nxl, grank * nxl, &s.plan,
-                  o.kernel == LBM_KERNEL_K3 ? 3 : 2);
+        const int bxi = j / by, byi = j % by;
+        const int grank = o.rank * sw + bxi;  // global x-slab index
+        fill_plan(nx, nyl, nz, c->esize, o.bc, grank, nslab_total, nxl, grank * nxl, &s.plan,
+                  o.kernel == LBM_KERNEL_K3 ? 3 : 2, by > 1);
         s.g.nx = nx;
-        s.g.ny = ny;
+        s.g.ny = nyl;
+        s.y0 = byi * nyl;
+        if (by > 1) {
+            const bool per = o.bc == LBM_BC_PERIODIC;
+            s.g.ylo_wall = !per && byi == 0;
+            s.g.yhi_wall = !per && byi == by - 1;
+            s.g.ywrap = 0;
+            const int dn = per ? (byi - 1 + by) % by : byi - 1, upi = per ? (byi + 1) % by : byi + 1;
+            s.down = dn >= 0 ? bxi * by + dn : -1;
+            s.up = upi < by ? bxi * by + upi : -1;
+        }
         s.g.nz = nz;
         s.g.nxl = nxl;
         s.g.x0 = grank * nxl;
@@ -1829,9 +2027,10 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
             s.left = s.plan.left;
             s.right = s.plan.right;
         } else {
-            // neighbours are local slab indices (a ring of the local slabs when periodic)
-            s.left = s.plan.left >= 0 ? s.plan.left - o.rank * sw : -1;
-            s.right = s.plan.right >= 0 ? s.plan.right - o.rank * sw : -1;
+            // neighbours are local slab indices (a ring of the local slabs when
+            // periodic; the same y block of the neighbouring x range)
+            s.left = s.plan.left >= 0 ? (s.plan.left - o.rank * sw) * by + byi : -1;
+            s.right = s.plan.right >= 0 ? (s.plan.right - o.rank * sw) * by + byi : -1;
         }
         const size_t bytes = size_t(s.g.pmod) * size_t(s.plan.plane_x) * c->esize;
         for (int b = 0; b < (c->sc || o.kernel == LBM_KERNEL_AA ? 1 : 2); ++b) {

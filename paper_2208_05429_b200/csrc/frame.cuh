@@ -20,7 +20,8 @@ struct FrameMask {
 
 __device__ __forceinline__ FrameMask frame_mask(const SlabGeom& g, int y, int z) {
     FrameMask m;
-    for (int j = 0; j < 2 * g.gy; ++j) {
+    // (X-Y blocks: a y-partitioned slab's frame rows are its neighbours' rows)
+    for (int j = 0; j < (g.ywrap ? 2 * g.gy : 0); ++j) {
         const int t = j < g.gy ? j - g.gy : g.ny + j - g.gy;
         if (((t % g.ny) + g.ny) % g.ny == y) m.rows |= 2u << j;
     }

@@ -229,7 +229,10 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     }
     const bool act1 = tid < C::HY * C::HZ;
     const int qy = y0 - 1 + a, qz = z0 - 1 + b;
-    const bool q_in = act1 && (BC == BC_PERIODIC || (qy >= 0 && qy < g.ny && qz >= 0 && qz < g.nz));
+    // (X-Y blocks: a y end that is not a domain wall has the neighbour's
+    // rows in the frame, so halo cells beyond it are real cells)
+    const int ymin = g.ylo_wall ? 0 : -2, ymax = g.yhi_wall ? g.ny : g.ny + 2;
+    const bool q_in = act1 && (BC == BC_PERIODIC || (qy >= ymin && qy < ymax && qz >= 0 && qz < g.nz));
     const bool q_tile = act1 && a >= 1 && a <= TY && b >= 1 && b <= TZ;
     // step-2 cell of this thread
     const int y2 = tid / TZ, z2 = tid % TZ;
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool warp2 = (tid & ~31) < TY * TZ;  // the warp owns step-2 cells (warp-uniform)
     const int st_off = (y0 + y2) * g.nzp + (z0 + z2);  // in-plane offset of the step-2 cell (< 2^31)
     // does any staged entry of this tile pull from outside [0,ny) x [0,nz)?
-    const bool edge_y = (y0 < 2) || (y0 + TY + 2 > g.ny);
+    const bool edge_y = (y0 < 2 && g.ylo_wall) || (y0 + TY + 2 > g.ny && g.yhi_wall);
     const bool edge_z = (z0 < 2) || (z0 + TZ + 2 > g.nz);
 
     // L2 policy of the staging loads: evict_last (default) keeps the rows a
@@ -287,7 +290,8 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     int wrow = -1, wcol = -1, wsy = 0, wsz = 0;  // wsy / wsz: c_y / c_z of the wall slots
     bool wb_ok = false;
     if constexpr (BC == BC_CAVITY) {
-        const int r0 = y0 <= 1 ? 1 - y0 : -1, r1 = (g.ny - y0 >= 0 && g.ny - y0 <= C::HY - 1) ? g.ny - y0 : -1;
+        const int r0 = (y0 <= 1 && g.ylo_wall) ? 1 - y0 : -1,
+                  r1 = (g.ny - y0 >= 0 && g.ny - y0 <= C::HY - 1 && g.yhi_wall) ? g.ny - y0 : -1;
         const int c0 = z0 <= 1 ? 1 - z0 : -1, c1 = (g.nz - z0 >= 0 && g.nz - z0 <= C::HZ - 1) ? g.nz - z0 : -1;
         wb_ok = edge_tile && !(r0 >= 0 && r1 >= 0) && !(c0 >= 0 && c1 >= 0);
         if (r0 >= 0) { wrow = r0; wsy = 1; } else if (r1 >= 0) { wrow = r1; wsy = -1; }
@@ -412,8 +416,8 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                             bool wall = false;
                             if constexpr (cx == 1) wall = wall || lwall;
                             if constexpr (cx == -1) wall = wall || rwall;
-                            if constexpr (cy == 1) wall = wall || qy == 0;
-                            if constexpr (cy == -1) wall = wall || qy == g.ny - 1;
+                            if constexpr (cy == 1) wall = wall || (qy == 0 && g.ylo_wall);
+                            if constexpr (cy == -1) wall = wall || (qy == g.ny - 1 && g.yhi_wall);
                             if constexpr (cz == 1) wall = wall || qz == 0;
                             if constexpr (cz == -1) wall = wall || qz == g.nz - 1;
                             if (wall) {
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                             constexpr int i = slot_dir(k);
                             constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
                             const int sy = qy - cy, sz = qz - cz;
-                            bool out = sy < 0 || sy >= g.ny || sz < 0 || sz >= g.nz;
+                            bool out = (sy < 0 && g.ylo_wall) || (sy >= g.ny && g.yhi_wall) || sz < 0 || sz >= g.nz;
                             if constexpr (cx == 1) out = out || lwall;
                             if constexpr (cx == -1) out = out || rwall;
                             if (out) {
@@ -666,9 +670,9 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     // Cavity: the cells only, so boxes reaching past a wall are zero-filled
     // (the wall lanes substitute those entries).  Periodic: the whole plane
     // including the ghost frame, from the buffer base (A is the cell origin).
-    const bool frame = g.gy > 0;
+    // (X-Y cavity blocks: frame rows but no frame columns -- z stays zero-filled)
     const T* const base = A - g.org;
-    const cuuint64_t dims[3] = {cuuint64_t(frame ? g.nzp : g.nz), cuuint64_t(g.ny + 2 * g.gy),
+    const cuuint64_t dims[3] = {cuuint64_t(g.zoff ? g.nzp : g.nz), cuuint64_t(g.ny + 2 * g.gy),
                                 cuuint64_t(g.pmod) * kQ};
     const cuuint64_t strides[2] = {cuuint64_t(g.nzp) * sizeof(T), cuuint64_t(g.pq) * sizeof(T)};
     const cuuint32_t box[3] = {cuuint32_t(C::BW), cuuint32_t(C::HY), 1u};

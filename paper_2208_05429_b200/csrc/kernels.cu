@@ -101,7 +101,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_frame_fill(T* __restrict__ F, SlabGeom g) {
     const int x = int(blockIdx.y) / kQ, k = int(blockIdx.y) % kQ;
     T* const P = F + plane_base(g, x) + (long long)k * g.pq;
-    const int S = g.zoff, W = g.nz + 2 * S, nrow = 2 * g.gy * W, n = nrow + 2 * S * g.ny;
+    // (X-Y blocks: the frame rows are the y-neighbours' rows -- exchanged)
+    const int S = g.zoff, W = g.nz + 2 * S, nrow = g.ywrap ? 2 * g.gy * W : 0, n = nrow + 2 * S * g.ny;
     for (int e = int(blockIdx.x * blockDim.x + threadIdx.x); e < n; e += int(gridDim.x * blockDim.x)) {
         int y, z;
         if (e < nrow) {
@@ -120,8 +121,8 @@ __global__ void __launch_bounds__(256) k_frame_fill(T* __restrict__ F, SlabGeom 
 
 template <typename T>
 cudaError_t launch_frame_fill(T* F, const SlabGeom& g, cudaStream_t s) {
-    if (g.gy == 0 || g.nxl <= 0) return cudaSuccess;
-    const int n = 2 * g.gy * (g.nz + 2 * g.zoff) + 2 * g.zoff * g.ny;
+    if (g.gy == 0 || g.nxl <= 0 || (!g.ywrap && g.zoff == 0)) return cudaSuccess;
+    const int n = (g.ywrap ? 2 * g.gy * (g.nz + 2 * g.zoff) : 0) + 2 * g.zoff * g.ny;
     k_frame_fill<T><<<dim3(unsigned((n + 255) / 256), unsigned(g.nxl * kQ)), 256, 0, s>>>(F, g);
     return cudaGetLastError();
 }
@@ -168,13 +169,13 @@ __device__ __forceinline__ T unstream_slot(const T* C, const StepParams<T>& P, i
     if constexpr (BC == BC_CAVITY) {
         if constexpr (cx == -1) wall = wall || (x == 0 && g.left_wall);
         if constexpr (cx == 1) wall = wall || (x == g.nxl - 1 && g.right_wall);
-        if constexpr (cy == -1) wall = wall || (y == 0);
-        if constexpr (cy == 1) wall = wall || (y == g.ny - 1);
+        if constexpr (cy == -1) wall = wall || (y == 0 && g.ylo_wall);
+        if constexpr (cy == 1) wall = wall || (y == g.ny - 1 && g.yhi_wall);
         if constexpr (cz == -1) wall = wall || (z == 0);
         if constexpr (cz == 1) wall = wall || (z == g.nz - 1);
     } else {
-        if constexpr (cy == -1) ty = (y == 0) ? g.ny - 1 : ty;
-        if constexpr (cy == 1) ty = (y == g.ny - 1) ? 0 : ty;
+        if constexpr (cy == -1) ty = (y == 0 && g.ywrap) ? g.ny - 1 : ty;
+        if constexpr (cy == 1) ty = (y == g.ny - 1 && g.ywrap) ? 0 : ty;
         if constexpr (cz == -1) tz = (z == 0) ? g.nz - 1 : tz;
         if constexpr (cz == 1) tz = (z == g.nz - 1) ? 0 : tz;
     }

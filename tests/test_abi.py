@@ -139,6 +139,29 @@ def test_lattice_validation():
         lbm.lbm_lattice_table(21)
 
 
+def test_xy_blocks_validation():
+    """X-Y blocks (local_blocks_y) need LOCAL slabs, ny divisible into >= 4
+    rows per block, and the two-buffer K1/K2 storage."""
+    o = lbm.lbm_default_opts()
+    assert o.local_blocks_y == 1
+    o.local_blocks_y = 2
+    with pytest.raises(lbm.LbmError, match="comm LOCAL"):
+        lbm.lbm_create_ex(8, 16, 8, 0.6, None, "f64", o)
+    o.comm = lbm.LBM_COMM_LOCAL
+    o.local_blocks_y = 3
+    with pytest.raises(lbm.LbmError, match="rows each"):
+        lbm.lbm_create_ex(8, 16, 8, 0.6, None, "f64", o)
+    o.local_blocks_y = 8
+    with pytest.raises(lbm.LbmError, match="rows each"):
+        lbm.lbm_create_ex(8, 16, 8, 0.6, None, "f64", o)
+    o.local_blocks_y, o.kernel = 2, lbm.LBM_KERNEL_AA
+    with pytest.raises(lbm.LbmError, match="two-buffer"):
+        lbm.lbm_create_ex(8, 16, 8, 0.6, None, "f64", o)
+    o.kernel, o.lattice = lbm.LBM_KERNEL_AUTO, 27
+    with pytest.raises(lbm.LbmError, match="D3Q27"):
+        lbm.lbm_create_ex(8, 16, 8, 0.6, None, "f64", o)
+
+
 def test_header_enums_match_binding():
     """Every enumerator of include/lbm.h has the same value in the binding."""
     src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "lbm.h")).read(), flags=re.S)

@@ -260,6 +260,45 @@ def test_k3_three_step_bitwise(dims):
     assert relerr_floor(res[1][-1], oracle.run(f0, lbm.LBM_BC_PERIODIC, 0.6, LID, 16)) <= TOL["f32"] * 16
 
 
+@pytest.mark.parametrize("bx,by", [(1, 2), (2, 2), (1, 4), (3, 2)])
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_xy_blocks_bitwise(bx, by, bc, dtype):
+    """X-Y partition emulated on one
+    GPU: bx x-ranges times by y-blocks, frame rows exchanged between blocks,
+    then the x ghost planes -- the same bits as one slab for K2 sweeps, K1
+    steps and read-backs in between (populations, boxes across block seams,
+    moments), from host and device initial fields, and the oracle."""
+    dims = (12, 16, 40)
+    f0 = li.random_populations(37, *dims)
+    rho = 1.0 + li.uniform(38, int(np.prod(dims)), -1e-3, 1e-3).reshape(dims)
+    u = li.uniform(39, 3 * int(np.prod(dims)), -0.01, 0.01).reshape(*dims, 3)
+    res = []
+    for kw in ({}, dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=bx, local_blocks_y=by)):
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=bc, **kw) as lat:
+            out = []
+            lat.set_populations(f0)
+            for n in (3, 2, 4, 1, 2):
+                lat.step(n)
+                out.append(lat.populations())
+                out.extend(lat.macroscopic())
+                out.append(lat.populations_box(2, 5, 3, 7, 9, 30))
+            lat.init_equilibrium(rho, u)
+            lat.step(5)
+            out.append(lat.populations())
+            lbm.lbm_init_equilibrium_device(lat.ctx, torch.from_numpy(rho).cuda(), torch.from_numpy(u).cuda())
+            lat.step(4)
+            r = torch.empty(dims, dtype=torch.float64, device="cuda")
+            v = torch.empty(*dims, 3, dtype=torch.float64, device="cuda")
+            lbm.lbm_macroscopic_device(lat.ctx, r, v)
+            lbm.lbm_synchronize(lat.ctx)
+            out.extend([r.cpu().numpy(), v.cpu().numpy(), lat.populations()])
+            res.append(out)
+    for a, b in zip(*res):
+        assert np.array_equal(a, b), (bx, by, bc, dtype)
+    assert relerr_floor(res[1][0], oracle.run(f0, bc, 0.6, LID, 3)) <= TOL[dtype]
+
+
 K2_VARIANTS = [("LBM_K2_TILE", v, 2) for v in ["8x32", "8x16", "16x16"]] + [("LBM_K2_EARLY", "0", 2), ("LBM_K2_CHUNK", "3", 2)]
 
 

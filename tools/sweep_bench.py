@@ -25,6 +25,7 @@ ap.add_argument("--steps", type=int, default=40)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tag", default="")
 ap.add_argument("--slabs", type=int, default=1, help="LOCAL X-slabs on this GPU (exchange path)")
+ap.add_argument("--blocks-y", type=int, default=1, help="LOCAL: also split every x slab into this many y blocks")
 ap.add_argument("--power", action="store_true", help="also sample SM clock and board power (NVML)")
 ap.add_argument("--lattice", type=int, default=19, help="19, or 15 / 27 (one-step kernel)")
 a = ap.parse_args()
@@ -32,7 +33,8 @@ nx, ny, nz = (int(v) for v in a.dims.split(","))
 kern = {"auto": 0, "k1": 1, "k2": 2, "aa": 4, "k2sc": 5, "k3": 6}[a.kernel]
 bc = lbm.LBM_BC_CAVITY if a.bc == "cavity" else lbm.LBM_BC_PERIODIC
 es = 8 if a.dtype == "f64" else 4
-kw = dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=a.slabs) if a.slabs > 1 else {}
+kw = (dict(comm=lbm.LBM_COMM_LOCAL, local_slabs=a.slabs, local_blocks_y=a.blocks_y)
+      if a.slabs > 1 or a.blocks_y > 1 else {})
 with lbm.Lattice(nx, ny, nz, 0.6, (0.05, 0, 0), a.dtype, bc=bc, kernel=kern, lattice=a.lattice, **kw) as lat:
     lat.init_equilibrium(None, None)
     lat.step(4)
