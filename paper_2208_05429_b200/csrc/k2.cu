@@ -14,9 +14,11 @@
 //      mbarrier, double-buffered).  Each thread reads its 19 values into
 //      registers, then ONE block barrier frees the buffer and the TMA of
 //      plane p+2 is issued before any collision, so every load has two
-//      compute phases to land.  Entries whose source lies beyond a wall
-//      (bounce-back + lid) or wraps (periodic) are replaced per thread in
-//      registers with an ordinary load -- no CTA-wide fix-up pass.
+//      compute phases to land.  Entries whose source lies beyond a cavity
+//      wall (bounce-back + lid) are replaced per thread in registers -- no
+//      CTA-wide fix-up pass.  A periodic box never wraps here: its planes
+//      carry a ghost frame of the wrapped rows / columns (frame.cuh) that
+//      the boxes read and this kernel's own stores keep current.
 //   2. Step 1: every cell of T+1 collides (BGK, registers) and PUSHES its
 //      post-collision populations into a destination-indexed SMEM ring:
 //      direction i goes to the cell it streams to, (p + c_x, y + c_y, z + c_z).
@@ -29,7 +31,7 @@
 // The ring keeps, per destination plane, only the populations still to
 // arrive: c_x = -1 group (5) x 2 planes, c_x = 0 (9) x 3, c_x = +1 (5) x 4.
 // Every population therefore crosses HBM once per two steps (plus the halo
-// re-reads that miss L2: 1.13-1.18x the algorithmic reads, ncu).
+// re-reads that miss L2: 1.1-1.25x the algorithmic reads, ncu).
 //
 // The arithmetic is the same bgk_collide()/pull rules as K1 (d3q19.cuh), so
 // K2 == K1 o K1 bit for bit (tests/test_gpu_parity.py).
@@ -141,7 +143,7 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m
 
 }  // namespace
 
-template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
+template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING, bool YB>
 __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     k2_sweep(const __grid_constant__ CUtensorMap tmA, const T* __restrict__ A, T* __restrict__ B, StepParams<T> P,
              int xbeg, int xend, int chunk, int out_poff, unsigned* __restrict__ sc_sync, T* haloL, T* haloR,
@@ -231,7 +233,11 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const int qy = y0 - 1 + a, qz = z0 - 1 + b;
     // (X-Y blocks: a y end that is not a domain wall has the neighbour's
     // rows in the frame, so halo cells beyond it are real cells)
-    const int ymin = g.ylo_wall ? 0 : -2, ymax = g.yhi_wall ? g.ny : g.ny + 2;
+    // (YB: an X-Y block, whose y ends are walls only where they are the
+    // domain's; otherwise compile-time walls -- the flags cost the plain
+    // cavity sweep 2-3% as runtime values)
+    const bool ylo = YB ? g.ylo_wall != 0 : true, yhi = YB ? g.yhi_wall != 0 : true;
+    const int ymin = ylo ? 0 : -2, ymax = yhi ? g.ny : g.ny + 2;
     const bool q_in = act1 && (BC == BC_PERIODIC || (qy >= ymin && qy < ymax && qz >= 0 && qz < g.nz));
     const bool q_tile = act1 && a >= 1 && a <= TY && b >= 1 && b <= TZ;
     // step-2 cell of this thread
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool warp2 = (tid & ~31) < TY * TZ;  // the warp owns step-2 cells (warp-uniform)
     const int st_off = (y0 + y2) * g.nzp + (z0 + z2);  // in-plane offset of the step-2 cell (< 2^31)
     // does any staged entry of this tile pull from outside [0,ny) x [0,nz)?
-    const bool edge_y = (y0 < 2 && g.ylo_wall) || (y0 + TY + 2 > g.ny && g.yhi_wall);
+    const bool edge_y = (y0 < 2 && ylo) || (y0 + TY + 2 > g.ny && yhi);
     const bool edge_z = (z0 < 2) || (z0 + TZ + 2 > g.nz);
 
     // L2 policy of the staging loads: evict_last (default) keeps the rows a
@@ -290,8 +296,8 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     int wrow = -1, wcol = -1, wsy = 0, wsz = 0;  // wsy / wsz: c_y / c_z of the wall slots
     bool wb_ok = false;
     if constexpr (BC == BC_CAVITY) {
-        const int r0 = (y0 <= 1 && g.ylo_wall) ? 1 - y0 : -1,
-                  r1 = (g.ny - y0 >= 0 && g.ny - y0 <= C::HY - 1 && g.yhi_wall) ? g.ny - y0 : -1;
+        const int r0 = (y0 <= 1 && ylo) ? 1 - y0 : -1,
+                  r1 = (g.ny - y0 >= 0 && g.ny - y0 <= C::HY - 1 && yhi) ? g.ny - y0 : -1;
         const int c0 = z0 <= 1 ? 1 - z0 : -1, c1 = (g.nz - z0 >= 0 && g.nz - z0 <= C::HZ - 1) ? g.nz - z0 : -1;
         wb_ok = edge_tile && !(r0 >= 0 && r1 >= 0) && !(c0 >= 0 && c1 >= 0);
         if (r0 >= 0) { wrow = r0; wsy = 1; } else if (r1 >= 0) { wrow = r1; wsy = -1; }
@@ -416,8 +422,8 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                             bool wall = false;
                             if constexpr (cx == 1) wall = wall || lwall;
                             if constexpr (cx == -1) wall = wall || rwall;
-                            if constexpr (cy == 1) wall = wall || (qy == 0 && g.ylo_wall);
-                            if constexpr (cy == -1) wall = wall || (qy == g.ny - 1 && g.yhi_wall);
+                            if constexpr (cy == 1) wall = wall || (qy == 0 && ylo);
+                            if constexpr (cy == -1) wall = wall || (qy == g.ny - 1 && yhi);
                             if constexpr (cz == 1) wall = wall || qz == 0;
                             if constexpr (cz == -1) wall = wall || qz == g.nz - 1;
                             if (wall) {
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                             constexpr int i = slot_dir(k);
                             constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
                             const int sy = qy - cy, sz = qz - cz;
-                            bool out = (sy < 0 && g.ylo_wall) || (sy >= g.ny && g.yhi_wall) || sz < 0 || sz >= g.nz;
+                            bool out = (sy < 0 && ylo) || (sy >= g.ny && yhi) || sz < 0 || sz >= g.nz;
                             if constexpr (cx == 1) out = out || lwall;
                             if constexpr (cx == -1) out = out || rwall;
                             if (out) {
@@ -643,12 +649,12 @@ constexpr int k2_max_chunk(bool wide = false) {
     return sizeof(T) == 8 ? (wide ? 56 : 32) : 48;
 }
 
-template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING>
+template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING, bool YB = false>
 cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, int nxs, int out_poff,
                            unsigned* sc_sync, T* haloL, T* haloR, cudaStream_t s, int xbeg2 = 0, int nxs2 = 0) {
     using C = K2Cfg<T, TY, TZ>;
     constexpr int NT = C::NT;
-    auto kern = k2_sweep<T, BC, TY, TZ, EARLY, RING>;
+    auto kern = k2_sweep<T, BC, TY, TZ, EARLY, RING, YB>;
     // The large-shared-memory opt-in is a per-device (per-context) function
     // attribute: set it once per device ordinal this process launches on
     // (setting it twice from racing threads is harmless).
@@ -790,8 +796,14 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
         return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, true>(A, B, P, xbeg, nxs, out_poff, sc_sync, nullptr, nullptr, s)
                    : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, true>(A, B, P, xbeg, nxs, out_poff, sc_sync, nullptr, nullptr, s);
     }
+    // X-Y blocks: the y-block kernel variants (EARLY issue order only)
+    const bool yb = !P.g.ylo_wall || !P.g.yhi_wall || !P.g.ywrap;
+    if (yb && !early) return cudaErrorNotSupported;
 #define LBM_K2_TILE_CASE(TY, TZ)                                                                              \
     if constexpr (K2Cfg<T, TY, TZ>::FITS) {                                                                   \
+        if (yb)                                                                                               \
+            return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, false, true>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s, xbeg2, nxs2) \
+                       : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, false, true>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s, xbeg2, nxs2);  \
         if (early)                                                                                            \
             return per ? launch_k2_impl<T, BC_PERIODIC, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s, xbeg2, nxs2) \
                        : launch_k2_impl<T, BC_CAVITY, TY, TZ, true, false>(A, B, P, xbeg, nxs, 0, nullptr, halo_left, halo_right, s, xbeg2, nxs2);  \

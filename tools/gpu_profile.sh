@@ -1,18 +1,24 @@
-# ncu evidence for profiles/ (run under gpurun): one config-5 sweep launch of K2 (fp64, fp32) and K1
-# under ncu --set full, and the launch list of the default bench command.
+# ncu evidence for profiles/ (run under gpurun; one GPU): one sweep launch per
+# kernel/workload under ncu --set full, and the launch list of the default
+# bench command.  Summaries: python tools/ncu_summary.py rep gpurun_out/<name>.ncu-rep
+# (round 2 captures: profiles/r02_*).
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+R=${R:-r02}
+cap() {  # cap <name> <kernel regex> <skip> <sweep_bench args...>
+  local name=$1 kre=$2 skip=$3; shift 3
+  local CMD="python tools/sweep_bench.py --steps 2 --reps 1 $*"
+  $CMD > gpurun_out/plain_$name.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:$kre -s $skip -c 1 -o gpurun_out/${R}_$name $CMD \
+    > gpurun_out/ncu_$name.log 2>&1
+}
 for dt in f64 f32; do
-  CMD="python tools/sweep_bench.py --dims 1024,512,512 --steps 2 --reps 1 --kernel k2 --dtype $dt"
-  $CMD > gpurun_out/plain_$dt.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:k2_sweep -s 2 -c 1 -o gpurun_out/r01_k2_${dt}_cfg5 $CMD > gpurun_out/ncu_k2_$dt.log 2>&1
+  cap k2_${dt}_cfg5 k2_sweep 2 --dims 1024,512,512 --kernel k2 --dtype $dt
+  cap k2_${dt}_cfg3 k2_sweep 2 --dims 256,256,256 --bc periodic --kernel k2 --dtype $dt
 done
-CMD="python tools/sweep_bench.py --dims 1024,512,512 --steps 2 --reps 1 --kernel k2sc --dtype f64"
-$CMD > gpurun_out/plain_k2sc.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k2_sweep -s 2 -c 1 -o gpurun_out/r01_k2sc_f64_cfg5 $CMD > gpurun_out/ncu_k2sc.log 2>&1
-CMD="python tools/sweep_bench.py --dims 1024,512,512 --steps 2 --reps 1 --kernel k1 --dtype f64"
-$CMD > gpurun_out/plain_k1.log 2>&1 && \
-ncu --set full --clock-control none -k regex:k1_step -s 4 -c 1 -o gpurun_out/r01_k1_f64_cfg5 $CMD > gpurun_out/ncu_k1.log 2>&1
+LBM_K2_TILE=8x32 cap k2_f32_cfg5_8x32 k2_sweep 2 --dims 1024,512,512 --kernel k2 --dtype f32
+cap k3_f32_cfg3 k3_sweep 1 --dims 256,256,256 --bc periodic --kernel k3 --dtype f32 --steps 3
+cap dqq27_f64_cfg4 k_dqq_step 3 --dims 512,512,512 --kernel k1 --dtype f64 --lattice 27
 BCMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
 $BCMD > gpurun_out/bench_ll_plain.json 2> gpurun_out/bench_ll_plain.err && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01_launches_bench_f64.csv $BCMD > gpurun_out/ncu_ll.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches_bench_f64.csv $BCMD > gpurun_out/ncu_ll.log 2>&1
 ls -la gpurun_out | tail -12
