@@ -175,7 +175,9 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "k1", "k2", "aa", "k2sc"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "k1", "k2", "aa", "k2sc", "k3"])
+    ap.add_argument("--halo", default="exchange", choices=["exchange", "peer"],
+                    help="N > 1: NCCL send/recv (default) or the fused peer-mapped halo (LBM_HALO_PEER)")
     ap.add_argument("--lbm-steps", type=int, default=None, help="time steps per job (default: the config's)")
     ap.add_argument("--dims", default=None, help="override NX,NY,NZ (profiling runs only)")
     ap.add_argument("--weak", action="store_true",
@@ -219,7 +221,7 @@ def main():
     cells_local = nxl * cfg.ny * cfg.nz
     stream = torch.cuda.Stream(device=dev)
     kernel = {"auto": lbm.LBM_KERNEL_AUTO, "k1": lbm.LBM_KERNEL_K1, "k2": lbm.LBM_KERNEL_K2,
-              "aa": lbm.LBM_KERNEL_AA, "k2sc": lbm.LBM_KERNEL_K2_SC}[args.kernel]
+              "aa": lbm.LBM_KERNEL_AA, "k2sc": lbm.LBM_KERNEL_K2_SC, "k3": lbm.LBM_KERNEL_K3}[args.kernel]
 
     nccl_id = None
     if world > 1:
@@ -230,7 +232,8 @@ def main():
         nccl_id = bytes(idt.cpu().numpy().tobytes())
     lat = lbm.Lattice(cfg.nx, cfg.ny, cfg.nz, cfg.tau, cfg.u_lid, args.dtype, bc=cfg.bc, kernel=kernel,
                       comm=lbm.LBM_COMM_NCCL if world > 1 else lbm.LBM_COMM_NONE, rank=rank, world=world,
-                      nccl_id=nccl_id, stream=stream.cuda_stream, device=local_rank)
+                      nccl_id=nccl_id, stream=stream.cuda_stream, device=local_rank,
+                      halo=lbm.LBM_HALO_PEER if (args.halo == "peer" and world > 1) else lbm.LBM_HALO_AUTO)
     ctx = lat.ctx
 
     # inputs: this rank's slab of the config's seeded fields, resident in HBM
@@ -304,7 +307,7 @@ def main():
     sweep_updates = s1.sweep_updates
     k2 = s1.k2_launches - s0.k2_launches
     k1 = s1.k1_launches - s0.k1_launches
-    dominant = (("k2_single_copy" if args.kernel == "k2sc" else "k2_two_step") if k2 >= k1
+    dominant = (({"k2sc": "k2_single_copy", "k3": "k3_three_step"}.get(args.kernel, "k2_two_step")) if k2 >= k1
                 else ("aa_step" if args.kernel == "aa" else "k1_step"))
     # per launch: cells_local x 2 x 19 x es bytes (both K1 and K2 stream the lattice once)
     bytes_per_launch = cells_local * 2 * 19 * es
@@ -366,6 +369,7 @@ def main():
                        "lbm_steps_per_job": cfg.steps, "job": "init_equilibrium + lbm_step(n) + macroscopic",
                        "inputs": ("rho (u is identically 0: passed as NULL)" if u_zero else "rho, u"),
                        "kernel": args.kernel, "parallelism": f"x-slab{world}",
+                       "halo": args.halo if world > 1 else "none",
                        "l2": f"inputs larger than L2: {cells_local * 19 * es / 1e9:.1f} GB per lattice copy per GPU"},
             "mlups_per_gpu": round(value / world, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
