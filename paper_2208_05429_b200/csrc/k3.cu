@@ -58,6 +58,14 @@ struct K3Cfg {
     static_assert(SMEM <= 227 * 1024, "K3 tile does not fit shared memory");
 };
 
+// one lane of a converged warp: single-thread TMA issue without the
+// compiler's per-copy election loop (see k2.cu elect_one)
+__device__ __forceinline__ bool k3_elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred px;\n\telect.sync _|px, 0xffffffff;\n\t@px mov.u32 %0, 1;\n\t}" : "+r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ uint32_t k3_smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -157,7 +165,7 @@ __global__ void __launch_bounds__(K3Cfg<T, TY, TZ>::NT, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) {
+    if (tid < 32 && k3_elect_one()) {
         issue(p_first, 0);
         issue(p_first + 1, 1);
     }
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(K3Cfg<T, TY, TZ>::NT, 1)
         }
         // stage free; rings of destination planes d1 (R1) and d2 (R2) complete
         __syncthreads();
-        if (tid == 0 && has1 && p + 2 <= p_last) issue(p + 2, s);
+        if (tid < 32 && has1 && p + 2 <= p_last && k3_elect_one()) issue(p + 2, s);
         if (has3 && act3) {
             const int t = a3 * TZ + b3;
             static_for<0, kQ>([&](auto kc) {
