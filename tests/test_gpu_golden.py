@@ -106,9 +106,10 @@ def _golden(cfg_id):
 
 
 @pytest.mark.parametrize("cfg_id,dtype,kernel", [(4, "f64", "auto"), (4, "f32", "auto"),
+                                                 (4, "f64", "k2sc"), (4, "f64", "aa"),
                                                  (5, "f64", "auto"), (5, "f32", "auto"),
                                                  (5, "f64", "k2sc"), (5, "f32", "k2sc"),
-                                                 (5, "f64", "aa")])
+                                                 (5, "f64", "aa"), (5, "f32", "aa")])
 def test_golden_configured_steps(cfg_id, dtype, kernel):
     """BASELINE.json:10-11 at full size, in the bench launch configuration,
     after the configured 100 steps: every stored population of the oracle's
