@@ -36,7 +36,8 @@ import paper_2208_05429_b200 as lbm  # noqa: E402
 
 TOL = {"f64": 1e-12, "f32": 1e-5}
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-KERNELS = {"auto": lbm.LBM_KERNEL_AUTO, "k2sc": lbm.LBM_KERNEL_K2_SC, "aa": lbm.LBM_KERNEL_AA}
+KERNELS = {"auto": lbm.LBM_KERNEL_AUTO, "k2sc": lbm.LBM_KERNEL_K2_SC, "aa": lbm.LBM_KERNEL_AA,
+           "k3": lbm.LBM_KERNEL_K3}
 
 
 def relerr(a, b):
@@ -66,10 +67,11 @@ def cfg3_oracle():
     return rho, u, f
 
 
-@pytest.mark.parametrize("dtype,kernel", [("f64", "auto"), ("f32", "auto"), ("f64", "k2sc")])
+@pytest.mark.parametrize("dtype,kernel", [("f64", "auto"), ("f32", "auto"), ("f64", "k2sc"), ("f32", "k3")])
 def test_config3_live_full_state(cfg3_oracle, dtype, kernel):
     """BASELINE.json:9: 256^3 periodic, 200 steps (the bench launch
-    configuration: K2 sweeps with the fused periodic halo), every population
+    configuration: K2 sweeps with the fused periodic halo; also the
+    single-copy ring and the three-step prototype K3), every population
     of every cell against the live oracle; the golden file written by
     tools/make_oracle_golden.py from the same oracle is bit-identical to it."""
     cfg = li.CONFIGS[3]
@@ -80,7 +82,8 @@ def test_config3_live_full_state(cfg3_oracle, dtype, kernel):
         assert lat.time == cfg.steps
         got = lat.populations()
         st = lbm.lbm_get_stats(lat.ctx)
-        assert st.k2_launches == cfg.steps // 2
+        # multi-step sweeps: 100 two-step (K2), or 66 three-step + one two-step (K3)
+        assert st.k2_launches == (cfg.steps // 3 + 1 if kernel == "k3" else cfg.steps // 2)
     assert relerr(got, ref) <= TOL[dtype]
     # momentum of the periodic box: conserved (oracle pin) and equal
     j_ref = np.array([np.sum(ref[i]) for i in range(19)])
