@@ -40,6 +40,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 
@@ -197,11 +198,27 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
         }
     };
     const int ntz = (g.nz + TZ - 1) / TZ;
-    // z-fastest tile order: z-neighbours (whose boxes share the 32 B halo
-    // sectors of every staged row) run together; a y-fastest order measured
-    // 1.33x the DRAM reads and -17% (config 5 fp64)
-    const int y0 = (item_t / ntz) * TY;
-    const int z0 = (item_t % ntz) * TZ;
+    // Tile order: z-fastest within strips of zbw tiles in z, then y, then
+    // the next strip.  z-neighbours (whose boxes share the 32 B halo sectors
+    // of every staged row) run together, and y-neighbours -- each re-stages
+    // a row of the other -- are only zbw tiles apart in the dispatch order,
+    // so they run within a few planes of each other and the shared rows are
+    // still in L2 (a y-fastest order measured 1.33x the DRAM reads, -17%).
+    int y0, z0;
+    {
+        const int zbw = min(max((kflags >> 8) & 0xff, 1), ntz);
+        const int nty = (g.ny + TY - 1) / TY;
+        const int full = ntz / zbw, inFull = full * nty * zbw;
+        if (item_t < inFull) {
+            const int sb = item_t / (nty * zbw), r = item_t - sb * (nty * zbw);
+            y0 = (r / zbw) * TY;
+            z0 = (sb * zbw + r % zbw) * TZ;
+        } else {
+            const int w = ntz - full * zbw, r = item_t - inFull;
+            y0 = (r / w) * TY;
+            z0 = (full * zbw + r % w) * TZ;
+        }
+    }
     // chunks [0, nch1) cover [xbeg, xend); chunks nch1.. the second range
     // [xbeg2, xbeg2 + xend - xbeg) (the two edge ranges of an overlapped sweep)
     const bool r2 = item_c >= nch1;
@@ -476,6 +493,8 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                 dslot = dslot >= g.pmod ? dslot - g.pmod : dslot;
             }
             T* const Bd = B + (long long)dslot * g.px;
+            // (32-bit slot offsets held in uniform registers -- 2 instead of
+            // 3 instructions per store address -- measured 1% slower)
             static_for<0, kQ>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
                 __stcs(Bd + (long long)k * g.pq + st_off, f2[slot_dir(k)]);
@@ -750,8 +769,18 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
         const char* e = getenv("LBM_K2_EVICT_LAST");  // A/B runs: 0 = evict_normal staging loads
         return (e && e[0] == '0') ? 0 : 1;
     }();
+    // tile-order strip width in z tiles (kernel comment): fp64 8 (config 5:
+    // DRAM reads 49.1 -> 46.7 GB per launch, +0.3% sustained; 4 and 2 lose
+    // more at the strip seams than they gain), fp32 whole rows (16x32
+    // tiles: 8 measured -0.5%).  LBM_K2_ZBLOCK overrides (tuning runs).
+    static const int zbw_env = [] {
+        const char* e = getenv("LBM_K2_ZBLOCK");
+        return e ? std::max(1, std::min(255, atoi(e))) : 0;
+    }();
+    const int zbw = zbw_env ? zbw_env : (sizeof(T) == 8 ? 8 : 255);
+
     kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk, out_poff, sc_sync, haloL, haloR, xbeg2,
-                                   nch1, l2last);
+                                   nch1, l2last | (zbw << 8));
     return cudaGetLastError();
 }
 

@@ -11,6 +11,8 @@ import time
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("LBM_PKG_ROOT"):  # A/B runs: a variant build of the package
+    sys.path.insert(0, os.environ["LBM_PKG_ROOT"])
 
 import numpy as np  # noqa: E402
 
