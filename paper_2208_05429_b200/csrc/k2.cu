@@ -4,7 +4,7 @@
 // the second collide").
 //
 // Each CTA owns an output tile T of TY x TZ cells in the (y, z) plane and
-// marches along x over a chunk of <= 32-56 planes (the paper's X-outermost
+// marches along x over a chunk of <= 32-72 planes (the paper's X-outermost
 // order; short chunks keep co-resident CTAs within a few planes
 // of each other, so the halo rows one CTA stages are still in L2 for its
 // neighbours).  Per input plane p:
@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const int toff = (a - 1) * TZ + (b - 1);        // ring entry of this cell (tile coords)
     // is the push destination (a - 1 + c_y, b - 1 + c_z) inside the tile, per c_y / c_z
     const bool rowok[3] = {a >= 2 && a <= TY + 1, a >= 1 && a <= TY, a <= TY - 1};
+    const bool row_mid = tid < C::HY * TZ && a >= 2 && a <= TY - 1;  // warp-uniform (TZ = 32)
     const bool colok[3] = {b >= 2 && b <= TZ + 1, b >= 1 && b <= TZ, b <= TZ - 1};
     const bool edge_tile = BC == BC_CAVITY && (edge_y || edge_z);
     // Cavity wall lanes of this tile: the box row holding y = 0 or y = ny-1
@@ -546,17 +547,33 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
             T (&f)[kQ] = fs;
             if (q_in) {
                 // ---- pushes: direction i streams to (p + cx, a - 1 + cy, b - 1 + cz) ----
-                static_for<0, kQ>([&](auto kc) {
+                auto push = [&](auto kc) {
                     constexpr int k = decltype(kc)::value;
                     constexpr int i = slot_dir(k);
-                    constexpr int cy = can_cy(i), cz = can_cz(i);
-                    constexpr int rel = cy * TZ + cz;
-                    if (rowok[cy + 1] && colok[cz + 1]) {
-                        if constexpr (k < 5) wM[k * C::RP + toff + rel] = f[i];
-                        else if constexpr (k < 14) wZ[(k - 5) * C::RP + toff + rel] = f[i];
-                        else wP[(k - 14) * C::RP + toff + rel] = f[i];
-                    }
-                });
+                    constexpr int rel = can_cy(i) * TZ + can_cz(i);
+                    if constexpr (k < 5) wM[k * C::RP + toff + rel] = f[i];
+                    else if constexpr (k < 14) wZ[(k - 5) * C::RP + toff + rel] = f[i];
+                    else wP[(k - 14) * C::RP + toff + rel] = f[i];
+                };
+#ifdef LBM_K2_ROWPUSH
+                if (row_mid) {
+                    // a warp of one tile row away from the tile's y edges
+                    // (warp-uniform): every c_y lands in the tile, so only the
+                    // first / last lane's c_z = -1 / +1 pushes are dropped
+                    const bool zlo = b >= 2, zhi = b <= TZ - 1;
+                    static_for<0, kQ>([&](auto kc) {
+                        constexpr int cz = can_cz(slot_dir(decltype(kc)::value));
+                        if (cz == 0 || (cz < 0 ? zlo : zhi)) push(kc);
+                    });
+                } else
+#endif
+                {
+                    static_for<0, kQ>([&](auto kc) {
+                        constexpr int i = slot_dir(decltype(kc)::value);
+                        constexpr int cy = can_cy(i), cz = can_cz(i);
+                        if (rowok[cy + 1] && colok[cz + 1]) push(kc);
+                    });
+                }
                 if constexpr (BC == BC_CAVITY) {
                     // ---- wall links of a tile cell: bounce-back (+ lid) into its own slot ----
                     if ((edge_tile || lwall || rwall) && q_tile) {
@@ -660,12 +677,12 @@ int num_sms() {
     return n;
 }
 
-// x chunks of at most k2_max_chunk planes (launch_k2_impl): fp64 56 on
+// x chunks of at most k2_max_chunk planes (launch_k2_impl): fp64 72 on
 // large cross-sections (`wide`), else 32 -- the single-copy ring always 32,
 // which sets its gap (k2_sc_gap); fp32 48
 template <typename T>
 constexpr int k2_max_chunk(bool wide = false) {
-    return sizeof(T) == 8 ? (wide ? 56 : 32) : 48;
+    return sizeof(T) == 8 ? (wide ? 72 : 32) : 48;
 }
 
 template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING, bool YB = false>
@@ -734,7 +751,9 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     // 1 kW power cap, and there the step-1 halo planes cost more than the
     // L2 misses: sustained config 5 32.2k at 32, 32.4k at 40, 32.5k at
     // 48-64, 29.9k at 128; config 4 32.2k -> 32.75k at 56.  So 56 where a
-    // chunk-plane holds >= 4 waves of tiles (configs 4, 5), else 32.
+    // chunk-plane holds >= 4 waves of tiles (configs 4, 5), else 32.  Round
+    // 2, with the z-strip tile order (less drift cost): the bench's K2 frac
+    // 0.784 at 56, 0.785 at 64, 0.789 at 72-88, 0.787 at 96 -> 72.
     const bool wide = !RING && ntiles >= 4 * slots;
     const int kMaxChunk = wide ? k2_max_chunk<T>(true) : k2_max_chunk<T>(false);
     int best = 1;
@@ -745,7 +764,10 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
         if (chunk > kMaxChunk && nch < nxs) continue;
         const long long items = ntiles * ((nxs + chunk - 1) / chunk) * ranges;
         const double waves = double((items + slots - 1) / slots);
-        const double cost = waves * (chunk + 2.5);
+        // per CTA: its planes (the average chunk), ~2.5 recomputed step-1
+        // planes and ~2 planes of pipeline fill (one CTA per SM: nothing
+        // overlaps a CTA's first TMA round trip)
+        const double cost = waves * (double(nxs) / nch + 2.5 + 2.0);
         if (cost < best_cost - 1e-9) {
             best_cost = cost;
             best = nch;
@@ -769,15 +791,16 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
         const char* e = getenv("LBM_K2_EVICT_LAST");  // A/B runs: 0 = evict_normal staging loads
         return (e && e[0] == '0') ? 0 : 1;
     }();
-    // tile-order strip width in z tiles (kernel comment): fp64 8 (config 5:
-    // DRAM reads 49.1 -> 46.7 GB per launch, +0.3% sustained; 4 and 2 lose
-    // more at the strip seams than they gain), fp32 whole rows (16x32
-    // tiles: 8 measured -0.5%).  LBM_K2_ZBLOCK overrides (tuning runs).
+    // tile-order strip width in z tiles (kernel comment): fp64 cavity 8
+    // (config 5: DRAM reads 49.1 -> 46.7 GB per launch, +0.3% sustained; 4
+    // and 2 lose more at the strip seams than they gain); fp32 (16x32
+    // tiles: 8 measured -0.5%) and periodic boxes (1024x512x512 fp64: -3%)
+    // whole rows.  LBM_K2_ZBLOCK overrides (tuning runs).
     static const int zbw_env = [] {
         const char* e = getenv("LBM_K2_ZBLOCK");
         return e ? std::max(1, std::min(255, atoi(e))) : 0;
     }();
-    const int zbw = zbw_env ? zbw_env : (sizeof(T) == 8 ? 8 : 255);
+    const int zbw = zbw_env ? zbw_env : ((sizeof(T) == 8 && BC == BC_CAVITY) ? 8 : 255);
 
     kern<<<grid, NT, C::SMEM, s>>>(map, A, B, P, xbeg, xbeg + nxs, chunk, out_poff, sc_sync, haloL, haloR, xbeg2,
                                    nch1, l2last | (zbw << 8));
