@@ -303,7 +303,6 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const int toff = (a - 1) * TZ + (b - 1);        // ring entry of this cell (tile coords)
     // is the push destination (a - 1 + c_y, b - 1 + c_z) inside the tile, per c_y / c_z
     const bool rowok[3] = {a >= 2 && a <= TY + 1, a >= 1 && a <= TY, a <= TY - 1};
-    const bool row_mid = tid < C::HY * TZ && a >= 2 && a <= TY - 1;  // warp-uniform (TZ = 32)
     const bool colok[3] = {b >= 2 && b <= TZ + 1, b >= 1 && b <= TZ, b <= TZ - 1};
     const bool edge_tile = BC == BC_CAVITY && (edge_y || edge_z);
     // Cavity wall lanes of this tile: the box row holding y = 0 or y = ny-1
@@ -547,33 +546,19 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
             T (&f)[kQ] = fs;
             if (q_in) {
                 // ---- pushes: direction i streams to (p + cx, a - 1 + cy, b - 1 + cz) ----
-                auto push = [&](auto kc) {
+                // (a warp-uniform branch for tile rows away from the y edges,
+                // whose pushes need only two lane predicates: -4%, reverted)
+                static_for<0, kQ>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
                     constexpr int i = slot_dir(k);
-                    constexpr int rel = can_cy(i) * TZ + can_cz(i);
-                    if constexpr (k < 5) wM[k * C::RP + toff + rel] = f[i];
-                    else if constexpr (k < 14) wZ[(k - 5) * C::RP + toff + rel] = f[i];
-                    else wP[(k - 14) * C::RP + toff + rel] = f[i];
-                };
-#ifdef LBM_K2_ROWPUSH
-                if (row_mid) {
-                    // a warp of one tile row away from the tile's y edges
-                    // (warp-uniform): every c_y lands in the tile, so only the
-                    // first / last lane's c_z = -1 / +1 pushes are dropped
-                    const bool zlo = b >= 2, zhi = b <= TZ - 1;
-                    static_for<0, kQ>([&](auto kc) {
-                        constexpr int cz = can_cz(slot_dir(decltype(kc)::value));
-                        if (cz == 0 || (cz < 0 ? zlo : zhi)) push(kc);
-                    });
-                } else
-#endif
-                {
-                    static_for<0, kQ>([&](auto kc) {
-                        constexpr int i = slot_dir(decltype(kc)::value);
-                        constexpr int cy = can_cy(i), cz = can_cz(i);
-                        if (rowok[cy + 1] && colok[cz + 1]) push(kc);
-                    });
-                }
+                    constexpr int cy = can_cy(i), cz = can_cz(i);
+                    constexpr int rel = cy * TZ + cz;
+                    if (rowok[cy + 1] && colok[cz + 1]) {
+                        if constexpr (k < 5) wM[k * C::RP + toff + rel] = f[i];
+                        else if constexpr (k < 14) wZ[(k - 5) * C::RP + toff + rel] = f[i];
+                        else wP[(k - 14) * C::RP + toff + rel] = f[i];
+                    }
+                });
                 if constexpr (BC == BC_CAVITY) {
                     // ---- wall links of a tile cell: bounce-back (+ lid) into its own slot ----
                     if ((edge_tile || lwall || rwall) && q_tile) {
