@@ -29,6 +29,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+if os.environ.get("LBM_PKG_ROOT"):  # A/B runs only: a variant build of the package (tools/build_variant.sh)
+    sys.path.insert(0, os.environ["LBM_PKG_ROOT"])
 
 import lbm_inputs as li  # noqa: E402
 

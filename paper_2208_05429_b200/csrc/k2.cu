@@ -305,6 +305,9 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
     const bool rowok[3] = {a >= 2 && a <= TY + 1, a >= 1 && a <= TY, a <= TY - 1};
     const bool colok[3] = {b >= 2 && b <= TZ + 1, b >= 1 && b <= TZ, b <= TZ - 1};
     const bool edge_tile = BC == BC_CAVITY && (edge_y || edge_z);
+    // this cell's cavity walls (a link from beyond: c_y = +1 at y = 0, ...)
+    const bool wyl = BC == BC_CAVITY && qy == 0 && ylo, wyh = BC == BC_CAVITY && qy == g.ny - 1 && yhi;
+    const bool wzl = BC == BC_CAVITY && qz == 0, wzh = BC == BC_CAVITY && qz == g.nz - 1;
     // Cavity wall lanes of this tile: the box row holding y = 0 or y = ny-1
     // and the box column holding z = 0 or z = nz-1 (at most one of each;
     // otherwise -- tiny domains -- the direct loads below).  Their wall-link
@@ -439,10 +442,10 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                             bool wall = false;
                             if constexpr (cx == 1) wall = wall || lwall;
                             if constexpr (cx == -1) wall = wall || rwall;
-                            if constexpr (cy == 1) wall = wall || (qy == 0 && ylo);
-                            if constexpr (cy == -1) wall = wall || (qy == g.ny - 1 && yhi);
-                            if constexpr (cz == 1) wall = wall || qz == 0;
-                            if constexpr (cz == -1) wall = wall || qz == g.nz - 1;
+                            if constexpr (cy == 1) wall = wall || wyl;
+                            if constexpr (cy == -1) wall = wall || wyh;
+                            if constexpr (cz == 1) wall = wall || wzl;
+                            if constexpr (cz == -1) wall = wall || wzh;
                             if (wall) {
                                 T v = A[self + (long long)slot_opp(k) * g.pq];
                                 if constexpr (cz == -1) {
@@ -567,14 +570,19 @@ __global__ void __launch_bounds__(K2Cfg<T, TY, TZ>::NT, K2Cfg<T, TY, TZ>::MINB)
                             constexpr int k = decltype(kc)::value;
                             constexpr int i = slot_dir(k);
                             constexpr int cx = can_cx(i), cy = can_cy(i), cz = can_cz(i);
-                            const int sy = qy - cy, sz = qz - cz;
-                            bool out = (sy < 0 && ylo) || (sy >= g.ny && yhi) || sz < 0 || sz >= g.nz;
+                            // the source x - c_i is beyond a wall: only the
+                            // cell's own wall flags in the directions c_i has
+                            bool out = false;
+                            if constexpr (cy == 1) out = out || wyl;
+                            if constexpr (cy == -1) out = out || wyh;
+                            if constexpr (cz == 1) out = out || wzl;
+                            if constexpr (cz == -1) out = out || wzh;
                             if constexpr (cx == 1) out = out || lwall;
                             if constexpr (cx == -1) out = out || rwall;
                             if (out) {
                                 T v = f[can_opp(i)];
                                 if constexpr (cz == -1) {
-                                    if (qz == g.nz - 1) v = v + P.lid[k];
+                                    if (wzh) v = v + P.lid[k];
                                 }
                                 if constexpr (k < 5) {
                                     heldP[k] = v;
