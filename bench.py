@@ -178,6 +178,8 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "k1", "k2", "aa", "k2sc", "k3"])
+    ap.add_argument("--ranks-y", type=int, default=1,
+                    help="N > 1 ranks as a (N / R) x R grid of X-Y blocks (lbm_opts.ranks_y; NCCL exchange)")
     ap.add_argument("--halo", default="exchange", choices=["exchange", "peer"],
                     help="N > 1: NCCL send/recv (default) or the fused peer-mapped halo (LBM_HALO_PEER)")
     ap.add_argument("--lbm-steps", type=int, default=None, help="time steps per job (default: the config's)")
@@ -218,9 +220,13 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
-    nxl = cfg.nx // world
-    x0 = rank * nxl
-    cells_local = nxl * cfg.ny * cfg.nz
+    ry = args.ranks_y if world > 1 else 1
+    if world % ry or cfg.ny % ry:
+        ap.error("--ranks-y must divide the world size and ny")
+    nxl = cfg.nx // (world // ry)
+    x0 = (rank // ry) * nxl
+    nyl, y0 = cfg.ny // ry, (rank % ry) * (cfg.ny // ry)
+    cells_local = nxl * nyl * cfg.nz
     stream = torch.cuda.Stream(device=dev)
     kernel = {"auto": lbm.LBM_KERNEL_AUTO, "k1": lbm.LBM_KERNEL_K1, "k2": lbm.LBM_KERNEL_K2,
               "aa": lbm.LBM_KERNEL_AA, "k2sc": lbm.LBM_KERNEL_K2_SC, "k3": lbm.LBM_KERNEL_K3}[args.kernel]
@@ -235,11 +241,15 @@ def main():
     lat = lbm.Lattice(cfg.nx, cfg.ny, cfg.nz, cfg.tau, cfg.u_lid, args.dtype, bc=cfg.bc, kernel=kernel,
                       comm=lbm.LBM_COMM_NCCL if world > 1 else lbm.LBM_COMM_NONE, rank=rank, world=world,
                       nccl_id=nccl_id, stream=stream.cuda_stream, device=local_rank,
-                      halo=lbm.LBM_HALO_PEER if (args.halo == "peer" and world > 1) else lbm.LBM_HALO_AUTO)
+                      halo=lbm.LBM_HALO_PEER if (args.halo == "peer" and world > 1) else lbm.LBM_HALO_AUTO,
+                      ranks_y=ry)
     ctx = lat.ctx
 
     # inputs: this rank's slab of the config's seeded fields, resident in HBM
     rho_h, u_h = li.init_fields(cfg, x0, nxl)
+    if ry > 1:  # this rank's X-Y block
+        rho_h = np.ascontiguousarray(rho_h[:, y0:y0 + nyl])
+        u_h = np.ascontiguousarray(u_h[:, y0:y0 + nyl])
     # A workload whose initial velocity is identically zero (the cavity
     # configs' recipe: rho = 1 + noise, u = 0) passes u = NULL, the API's
     # "u = 0" (include/lbm.h), instead of shipping 24 B of zeros per cell.
@@ -370,7 +380,7 @@ def main():
                        "bc": "periodic" if cfg.bc else "cavity", "tau": cfg.tau, "u_lid": list(cfg.u_lid),
                        "lbm_steps_per_job": cfg.steps, "job": "init_equilibrium + lbm_step(n) + macroscopic",
                        "inputs": ("rho (u is identically 0: passed as NULL)" if u_zero else "rho, u"),
-                       "kernel": args.kernel, "parallelism": f"x-slab{world}",
+                       "kernel": args.kernel, "parallelism": f"x-slab{world}" if ry == 1 else f"xy-block{world // ry}x{ry}",
                        "halo": args.halo if world > 1 else "none",
                        "l2": f"inputs larger than L2: {cells_local * 19 * es / 1e9:.1f} GB per lattice copy per GPU"},
             "mlups_per_gpu": round(value / world, 3),

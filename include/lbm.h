@@ -73,7 +73,7 @@
 extern "C" {
 #endif
 
-#define LBM_ABI_VERSION 2
+#define LBM_ABI_VERSION 3
 
 typedef struct lbm_ctx lbm_ctx; /* opaque; library-owned */
 
@@ -208,7 +208,9 @@ typedef struct {
     int struct_size;     /* sizeof(lbm_opts), for forward compatibility */
     int bc;              /* lbm_bc */
     int device;          /* CUDA device ordinal; -1 = the current device */
-    int rank, world;     /* X-slab partition: this process is slab `rank` of `world` */
+    int rank, world;     /* X-slab partition: this process is slab `rank` of `world`
+                            (host arrays: nx_local = nx / world planes, ny_local = ny rows;
+                            see ranks_y for X-Y blocks) */
     int comm;            /* lbm_comm */
     const void *nccl_id; /* 128-byte ncclUniqueId (same on all ranks) when comm == NCCL */
     void *stream;        /* cudaStream_t to run on, or NULL: the context creates one */
@@ -218,6 +220,13 @@ typedef struct {
     int lattice;         /* lbm_lattice: 19 (default; 0 reads as 19), 15 or 27 (ABI 2) */
     int local_blocks_y;  /* comm == LOCAL: also split every x slab into this many y blocks
                             (X-Y partition; 0 or 1 = none) (ABI 2) */
+    int ranks_y;         /* comm == NCCL: the world ranks form a (world / ranks_y) x ranks_y
+                            grid of X-Y blocks ("partition a 3D domain along
+                            three axes"): rank r holds x slab r / ranks_y (nx_local =
+                            nx / (world / ranks_y) planes) and y block r % ranks_y (ny_local =
+                            ny / ranks_y rows, >= 4); its host arrays cover that block,
+                            [nx_local][ny_local][nz].  Two-buffer K1/K2 storage (kernel AUTO,
+                            K1 or K2), halo EXCHANGE, D3Q19.  0 or 1 = X-slabs (ABI 3) */
 } lbm_opts;
 
 /* Fills *opts with defaults: CAVITY, device -1, rank 0, world 1, NONE,
@@ -239,8 +248,8 @@ lbm_status lbm_create_ex(lbm_ctx **out, int nx, int ny, int nz, double tau,
                          const double u_lid[3], lbm_dtype dtype, const lbm_opts *opts);
 
 /* f_i = feq_i(rho, u) on every cell of the slab (SPEC.md:74-82 with the
- * rest-population closure, R-2).  rho: host [nx_local][ny][nz]
- * or NULL (= 1); u: host [nx_local][ny][nz][3] or NULL (= 0).
+ * rest-population closure, R-2).  rho: host [nx_local][ny_local][nz]
+ * or NULL (= 1); u: host [nx_local][ny_local][nz][3] or NULL (= 0).
  * EINVAL if any rho <= 0 or any value is not finite. */
 lbm_status lbm_init_equilibrium(lbm_ctx *ctx, const double *rho, const double *u);
 /* Same with DEVICE pointers on the context's device (not validated). */
@@ -255,7 +264,7 @@ lbm_status lbm_step(lbm_ctx *ctx, long n);
 
 /* Moments of the canonical f(t): rho = sum_i f_i, u = (sum_i c_i f_i)/rho
  * (the paper's velocity norms).  Host arrays
- * rho [nx_local][ny][nz], u [nx_local][ny][nz][3]; either may be NULL.
+ * rho [nx_local][ny_local][nz], u [nx_local][ny_local][nz][3]; either may be NULL.
  * Blocks until the copy is complete.  ENUMERIC if some cell has rho == 0 or
  * non-finite moments (the arrays are still filled). */
 lbm_status lbm_macroscopic(lbm_ctx *ctx, double *rho, double *u);
@@ -263,14 +272,14 @@ lbm_status lbm_macroscopic(lbm_ctx *ctx, double *rho, double *u);
  * check: it would need a synchronisation). */
 lbm_status lbm_macroscopic_device(lbm_ctx *ctx, double *d_rho, double *d_u);
 
-/* Canonical populations f(t) as host f[q][nx_local][ny][nz] (canonical
+/* Canonical populations f(t) as host f[q][nx_local][ny_local][nz] (canonical
  * direction order; q = 19 unless opts.lattice says otherwise).  Blocks. */
 lbm_status lbm_get_populations(lbm_ctx *ctx, double *f);
 /* The box [x0,x0+lx) x [y0,y0+ly) x [z0,z0+lz) of the slab (slab-local x)
  * as host f[19][lx][ly][lz].  EINVAL if the box leaves the slab. */
 lbm_status lbm_get_populations_box(lbm_ctx *ctx, int x0, int y0, int z0, int lx,
                                    int ly, int lz, double *f);
-/* Set the canonical state f(t) from host f[q][nx_local][ny][nz].  EINVAL if
+/* Set the canonical state f(t) from host f[q][nx_local][ny_local][nz].  EINVAL if
  * a value is not finite. */
 lbm_status lbm_set_populations(lbm_ctx *ctx, const double *f);
 
@@ -310,10 +319,31 @@ typedef struct {
      * z_offset. */
     int y_ghost, z_offset;
     long long cell0;
+    /* X-Y blocks (lbm_plan_halo_xy, ABI 3; X-slabs: down = up = -1,
+     * ny_local = ny, y0 = 0).  The block's planes carry y_ghost = 2 frame
+     * rows per side (both boundary modes) holding the y-neighbours' edge
+     * rows.  Before every exchange of the x spans above, each rank sends the
+     * band of y_ghost rows (y_band = y_ghost * nz_pitch elements at offset
+     * send_down_off / send_up_off of every (x, direction) plane of its own
+     * planes x = 0 .. nx_local-1, i.e. 19 * nx_local bands at stride plane_q
+     * starting at plane x = 0) to its down / up neighbour, which stores them
+     * at recv_up_off / recv_down_off; the x spans then carry those rows to
+     * the x-neighbours, so the x-y corner entries come from the diagonal
+     * block without a diagonal message.  Ranks are numbered
+     * rank = x_slab * ranks_y + y_block; left/right above are ranks too. */
+    int down, up;            /* y-neighbour ranks or -1 (a cavity wall) */
+    int ny_local, y0;
+    long long y_band;
+    long long send_down_off, send_up_off, recv_down_off, recv_up_off;
 } lbm_halo_plan;
 
 lbm_status lbm_plan_halo(int nx, int ny, int nz, lbm_dtype dtype, int bc, int rank,
                          int world, lbm_halo_plan *plan);
+/* The same for a (world / ranks_y) x ranks_y rank grid of X-Y blocks
+ * (lbm_opts.ranks_y; ranks_y == 1 is lbm_plan_halo).  EINVAL: world %
+ * ranks_y != 0, nx % (world / ranks_y) != 0, ny % ranks_y != 0. */
+lbm_status lbm_plan_halo_xy(int nx, int ny, int nz, lbm_dtype dtype, int bc, int rank,
+                            int world, int ranks_y, lbm_halo_plan *plan);
 
 /* Diagnostics for the bench harness (no effect on results).
  * Kernel launches issued by this context since creation, and optional CUDA

@@ -49,7 +49,7 @@ class lbm_opts(ctypes.Structure):
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("comm", ctypes.c_int),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("kernel", ctypes.c_int),
                 ("local_slabs", ctypes.c_int), ("halo", ctypes.c_int), ("lattice", ctypes.c_int),
-                ("local_blocks_y", ctypes.c_int)]
+                ("local_blocks_y", ctypes.c_int), ("ranks_y", ctypes.c_int)]
 
 
 class lbm_halo_plan(ctypes.Structure):
@@ -59,7 +59,11 @@ class lbm_halo_plan(ctypes.Structure):
                 ("send_left_off", ctypes.c_longlong), ("send_right_off", ctypes.c_longlong),
                 ("recv_left_off", ctypes.c_longlong), ("recv_right_off", ctypes.c_longlong),
                 ("span", ctypes.c_longlong), ("dir_of_slot", ctypes.c_int * 19),
-                ("y_ghost", ctypes.c_int), ("z_offset", ctypes.c_int), ("cell0", ctypes.c_longlong)]
+                ("y_ghost", ctypes.c_int), ("z_offset", ctypes.c_int), ("cell0", ctypes.c_longlong),
+                ("down", ctypes.c_int), ("up", ctypes.c_int), ("ny_local", ctypes.c_int), ("y0", ctypes.c_int),
+                ("y_band", ctypes.c_longlong), ("send_down_off", ctypes.c_longlong),
+                ("send_up_off", ctypes.c_longlong), ("recv_down_off", ctypes.c_longlong),
+                ("recv_up_off", ctypes.c_longlong)]
 
 
 class lbm_stats(ctypes.Structure):
@@ -72,7 +76,7 @@ class lbm_stats(ctypes.Structure):
 EXPORTS = ["lbm_default_opts", "lbm_create", "lbm_create_ex", "lbm_init_equilibrium",
            "lbm_init_equilibrium_device", "lbm_step", "lbm_macroscopic", "lbm_macroscopic_device",
            "lbm_get_populations", "lbm_get_populations_box", "lbm_set_populations", "lbm_synchronize",
-           "lbm_get_time", "lbm_nccl_unique_id", "lbm_plan_halo", "lbm_profile_enable", "lbm_profile_reset",
+           "lbm_get_time", "lbm_nccl_unique_id", "lbm_plan_halo", "lbm_plan_halo_xy", "lbm_profile_enable", "lbm_profile_reset",
            "lbm_get_stats", "lbm_last_error", "lbm_destroy", "lbm_abi_version", "lbm_lattice_table"]
 
 
@@ -100,6 +104,7 @@ def _load():
         "lbm_get_time": (i, [ctxp, P(ctypes.c_long)]),
         "lbm_nccl_unique_id": (i, [vp]),
         "lbm_plan_halo": (i, [i, i, i, i, i, i, i, P(lbm_halo_plan)]),
+        "lbm_plan_halo_xy": (i, [i, i, i, i, i, i, i, i, P(lbm_halo_plan)]),
         "lbm_profile_enable": (i, [ctxp, i]),
         "lbm_profile_reset": (i, [ctxp]),
         "lbm_get_stats": (i, [ctxp, P(lbm_stats)]),
@@ -225,6 +230,13 @@ def lbm_plan_halo(nx, ny, nz, dtype, bc, rank, world) -> lbm_halo_plan:
     return p
 
 
+def lbm_plan_halo_xy(nx, ny, nz, dtype, bc, rank, world, ranks_y) -> lbm_halo_plan:
+    p = lbm_halo_plan()
+    dt = DTYPES[dtype] if isinstance(dtype, str) else int(dtype)
+    _check(_lib.lbm_plan_halo_xy(nx, ny, nz, dt, bc, rank, world, ranks_y, ctypes.byref(p)))
+    return p
+
+
 def lbm_profile_enable(ctx, on: bool):
     _check(_lib.lbm_profile_enable(ctx, 1 if on else 0), ctx)
 
@@ -267,18 +279,23 @@ class Lattice:
 
     def __init__(self, nx, ny, nz, tau, u_lid=(0.0, 0.0, 0.0), dtype="f64", bc=LBM_BC_CAVITY,
                  kernel=LBM_KERNEL_AUTO, comm=LBM_COMM_NONE, local_slabs=1, rank=0, world=1,
-                 nccl_id: bytes | None = None, stream=None, device=-1, halo=0, lattice=19, local_blocks_y=1):
+                 nccl_id: bytes | None = None, stream=None, device=-1, halo=0, lattice=19, local_blocks_y=1,
+                 ranks_y=1):
         o = lbm_default_opts()
         o.bc, o.kernel, o.comm, o.local_slabs, o.halo = bc, kernel, comm, local_slabs, halo
         o.lattice = lattice
         o.local_blocks_y = local_blocks_y
+        o.ranks_y = ranks_y
         self.q = lattice
         o.rank, o.world, o.device = rank, world, device
         self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         o.nccl_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None
         o.stream = stream
-        self.nx, self.ny, self.nz = nx, ny, nz
-        self.nx_local = nx // world
+        # host arrays cover this process's part: an x slab, or (ranks_y > 1)
+        # an X-Y block of ny // ranks_y rows
+        ry = max(1, ranks_y)
+        self.nx, self.ny, self.nz = nx, ny // ry, nz
+        self.nx_local = nx // (world // ry if world % ry == 0 else world)
         self.ctx = lbm_create_ex(nx, ny, nz, tau, u_lid, dtype, o)
 
     def init_equilibrium(self, rho=None, u=None):

@@ -121,6 +121,9 @@ struct lbm_ctx {
     // current: K2 sweeps keep it, every other writer clears it
     bool frame_valid = false;
     int yblocks = 1;  // X-Y blocks (LOCAL, local_blocks_y): slabs per x range, split along y
+    int ranks_y = 1;  // X-Y blocks across NCCL ranks (lbm_opts.ranks_y): this rank is one block
+    void* ypack = nullptr;  // NCCL X-Y: [send down | send up | recv down | recv up] row bands
+    size_t yband_bytes = 0;  // bytes of one of the four
     long t = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -368,6 +371,36 @@ void fill_plan(int nx, int ny, int nz, size_t esize, int bc, int rank, int world
     p->send_right_off = (long long)nxl * px + kSlotP0 * pq;
     p->span = (long long)kHaloSlots * pq;
     for (int k = 0; k < kQ; ++k) p->dir_of_slot[k] = slot_dir(k);
+    // X-Y blocks: the frame-row bands of an (x, direction) plane (plane rows
+    // r = y + y_ghost): own rows [0, gy) go down, [ny - gy, ny) go up; the
+    // frame rows [-gy, 0) come from down, [ny, ny + gy) from up
+    p->down = p->up = -1;
+    p->ny_local = ny;
+    p->y0 = 0;
+    p->y_band = (long long)p->y_ghost * p->nz_pitch;
+    p->send_down_off = (long long)p->y_ghost * p->nz_pitch;
+    p->send_up_off = (long long)ny * p->nz_pitch;
+    p->recv_down_off = 0;
+    p->recv_up_off = (long long)(p->y_ghost + ny) * p->nz_pitch;
+}
+
+// The plan of rank `rank` in a (world / ranks_y) x ranks_y grid of X-Y
+// blocks (lbm_opts.ranks_y): x slab rank / ranks_y, y block rank % ranks_y;
+// neighbours as ranks.  ranks_y == 1: fill_plan's X-slab plan.
+void fill_plan_xy(int nx, int ny, int nz, size_t esize, int bc, int rank, int world, int ranks_y,
+                  lbm_halo_plan* p) {
+    const int wx = world / ranks_y, bx = rank / ranks_y, byi = rank % ranks_y;
+    const int nxl = nx / wx, nyl = ny / ranks_y;
+    fill_plan(nx, nyl, nz, esize, bc, bx, wx, nxl, bx * nxl, p, 2, ranks_y > 1);
+    if (p->left >= 0) p->left = p->left * ranks_y + byi;
+    if (p->right >= 0) p->right = p->right * ranks_y + byi;
+    if (ranks_y > 1) {
+        const bool per = bc == LBM_BC_PERIODIC;
+        const int dn = per ? (byi - 1 + ranks_y) % ranks_y : byi - 1, upi = per ? (byi + 1) % ranks_y : byi + 1;
+        p->down = dn >= 0 ? bx * ranks_y + dn : -1;
+        p->up = upi < ranks_y ? bx * ranks_y + upi : -1;
+        p->y0 = byi * nyl;
+    }
 }
 
 bool finite_vec(const double* v) {
@@ -466,6 +499,36 @@ lbm_status exchange(lbm_ctx* c, int which, cudaStream_t st) {
         char* b = static_cast<char*>(s.buf[which]);
         const size_t es = c->esize;
         const ncclDataType_t ty = c->dt == LBM_F64 ? ncclFloat64 : ncclFloat32;
+        if (s.down >= 0 || s.up >= 0) {
+            // X-Y blocks across ranks: first the frame-row bands of the own
+            // planes with the y-neighbours (packed: one message per side),
+            // then the x spans below, which carry those rows along (the x-y
+            // corner entries come from the diagonal block); the same order
+            // as the LOCAL copies
+            const lbm_halo_plan& pl = s.plan;
+            char* const own = b + 2 * s.g.px * (long long)es;  // plane x = 0
+            const long long pqb = s.g.pq * (long long)es, bandb = pl.y_band * (long long)es;
+            const int nb = s.g.nxl * kQ;
+            char* const pk = static_cast<char*>(c->ypack);
+            char* const snd_dn = pk;
+            char* const snd_up = pk + c->yband_bytes;
+            char* const rcv_dn = pk + 2 * c->yband_bytes;
+            char* const rcv_up = pk + 3 * c->yband_bytes;
+            if (s.down >= 0) CK(launch_band_copy(own + pl.send_down_off * es, pqb, snd_dn, bandb, bandb, nb, st));
+            if (s.up >= 0) CK(launch_band_copy(own + pl.send_up_off * es, pqb, snd_up, bandb, bandb, nb, st));
+            const size_t n = size_t(nb) * size_t(pl.y_band);
+            CKN(g_nccl.GroupStart());
+            // [send down, recv up], [send up, recv down]: pairs match even
+            // when down == up (two y blocks in a ring, or this rank itself)
+            if (s.down >= 0) CKN(g_nccl.Send(snd_dn, n, ty, s.down, c->comm, st));
+            if (s.up >= 0) CKN(g_nccl.Recv(rcv_up, n, ty, s.up, c->comm, st));
+            if (s.up >= 0) CKN(g_nccl.Send(snd_up, n, ty, s.up, c->comm, st));
+            if (s.down >= 0) CKN(g_nccl.Recv(rcv_dn, n, ty, s.down, c->comm, st));
+            CKN(g_nccl.GroupEnd());
+            if (s.down >= 0) CK(launch_band_copy(rcv_dn, bandb, own + pl.recv_down_off * es, pqb, bandb, nb, st));
+            if (s.up >= 0) CK(launch_band_copy(rcv_up, bandb, own + pl.recv_up_off * es, pqb, bandb, nb, st));
+            c->launches += (s.down >= 0) * 2 + (s.up >= 0) * 2;
+        }
         const size_t n = size_t(s.plan.span);
         CKN(g_nccl.GroupStart());
         // order: [send left, recv right], [send right, recv left]: pairs match
@@ -598,6 +661,13 @@ bool aa_has_halo(const lbm_ctx* c) {
     if (c->slabs.size() == 1 && c->opts.world == 1) return false;
     for (const Slab& s : c->slabs)
         if (s.left >= 0 || s.right >= 0) return true;
+    return false;
+}
+
+// X-Y blocks (LOCAL or across NCCL ranks): some slab exchanges frame rows
+bool y_neighbours(const lbm_ctx* c) {
+    for (const Slab& s : c->slabs)
+        if (s.down >= 0 || s.up >= 0) return true;
     return false;
 }
 
@@ -822,7 +892,7 @@ lbm_status run_steps(lbm_ctx* c, long n) {
     // no exchange runs.  LBM_FUSED_HALO=0 turns it off (A/B runs, tests).
     // With NCCL ranks the same stores go into the neighbours' buffers as
     // mapped here (LBM_HALO_PEER, peer.cu).
-    const bool fuse = tma && c->fused_halo && (c->opts.comm != LBM_COMM_NCCL || c->peer) && c->yblocks == 1;
+    const bool fuse = tma && c->fused_halo && (c->opts.comm != LBM_COMM_NCCL || c->peer) && !y_neighbours(c);
     while (n > 0) {
         const int nsteps = (use_k2 && n >= 2) ? 2 : 1;
         const bool fused = fuse && nsteps == 2;
@@ -856,7 +926,7 @@ lbm_status run_steps(lbm_ctx* c, long n) {
             if (fst != LBM_OK) return fst;
         }
         const int h = nsteps;
-        bool split = !c->ghosts_valid && has_neighbours(c) && c->overlap && c->yblocks == 1;
+        bool split = !c->ghosts_valid && has_neighbours(c) && c->overlap && !y_neighbours(c);
         for (const Slab& s : c->slabs) split = split && s.g.nxl >= 2 * h + 2;
         if (!c->ghosts_valid && has_neighbours(c) && !split) {
             lbm_status st = exchange(c, c->cur, c->stream);
@@ -1355,7 +1425,7 @@ lbm_status init_eq(lbm_ctx* c, const double* rho, const double* u, bool host) {
             dr = rho ? rho + xoff : nullptr;
             du = u ? u + 3 * xoff : nullptr;
         }
-        if (c->slabs.size() == 1 && c->opts.world == 1) {
+        if (c->slabs.size() == 1 && c->opts.world == 1 && !y_neighbours(c)) {
             // one slab spanning the domain: the pull-form state in one pass
             // (k0_init_pull), the staging (host inputs) in the other buffer
             CK(launch_k0_init_pull<T>(dr, du, nullptr, origin<T>(s, canon), make_params<T>(c, s), 0,
@@ -1742,6 +1812,7 @@ void lbm_default_opts(lbm_opts* o) {
     o->halo = LBM_HALO_AUTO;
     o->lattice = 19;
     o->local_blocks_y = 1;
+    o->ranks_y = 1;
 }
 
 lbm_status lbm_lattice_table(int q, int* c, double* w) {
@@ -1762,6 +1833,21 @@ lbm_status lbm_lattice_table(int q, int* c, double* w) {
 }
 
 const char* lbm_last_error(const lbm_ctx* c) { return c ? c->err.c_str() : t_last_error.c_str(); }
+
+lbm_status lbm_plan_halo_xy(int nx, int ny, int nz, lbm_dtype dt, int bc, int rank, int world, int ranks_y,
+                            lbm_halo_plan* plan) {
+    lbm_ctx* c = nullptr;
+    if (!plan) return fail(c, LBM_EINVAL, "plan is NULL");
+    if (nx < 1 || ny < 1 || nz < 1) return fail(c, LBM_EINVAL, "dimensions must be >= 1");
+    if (dt != LBM_F64 && dt != LBM_F32) return fail(c, LBM_EINVAL, "bad dtype");
+    if (bc != LBM_BC_CAVITY && bc != LBM_BC_PERIODIC) return fail(c, LBM_EINVAL, "bad bc");
+    if (world < 1 || rank < 0 || rank >= world) return fail(c, LBM_EINVAL, "rank %d / world %d", rank, world);
+    if (ranks_y < 1 || world % ranks_y) return fail(c, LBM_EINVAL, "world %% ranks_y != 0");
+    if (nx % (world / ranks_y)) return fail(c, LBM_EINVAL, "nx %% (world / ranks_y) != 0");
+    if (ny % ranks_y) return fail(c, LBM_EINVAL, "ny %% ranks_y != 0");
+    fill_plan_xy(nx, ny, nz, dt == LBM_F64 ? 8 : 4, bc, rank, world, ranks_y, plan);
+    return LBM_OK;
+}
 
 lbm_status lbm_plan_halo(int nx, int ny, int nz, lbm_dtype dt, int bc, int rank, int world, lbm_halo_plan* plan) {
     lbm_ctx* c = nullptr;
@@ -1826,6 +1912,15 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         if (o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K1 && o.kernel != LBM_KERNEL_K2)
             return fail(c, LBM_EINVAL, "X-Y blocks run the two-buffer K1/K2 storage (kernel AUTO, K1 or K2)");
     }
+    const int ry = o.ranks_y < 1 ? 1 : o.ranks_y;
+    if (ry > 1) {
+        if (o.comm != LBM_COMM_NCCL) return fail(c, LBM_EINVAL, "ranks_y > 1 (X-Y blocks across ranks) needs comm NCCL");
+        if (o.world % ry) return fail(c, LBM_EINVAL, "world %d not divisible by ranks_y %d", o.world, ry);
+        if (ny % ry || ny / ry < 4) return fail(c, LBM_EINVAL, "ranks_y: ny %% ranks_y == 0, >= 4 rows per block");
+        if (o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K1 && o.kernel != LBM_KERNEL_K2)
+            return fail(c, LBM_EINVAL, "ranks_y > 1 runs the two-buffer K1/K2 storage (kernel AUTO, K1 or K2)");
+        if (o.halo == LBM_HALO_PEER) return fail(c, LBM_EINVAL, "ranks_y > 1 exchanges through NCCL (halo EXCHANGE)");
+    }
     const int q = o.lattice == 0 ? 19 : o.lattice;
     if (q != 15 && q != 19 && q != 27) return fail(c, LBM_EINVAL, "bad lattice %d (15, 19 or 27)", o.lattice);
     if (q != 19 && (o.comm != LBM_COMM_NONE || o.halo != LBM_HALO_AUTO || by > 1 ||
@@ -1840,7 +1935,7 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     if (o.kernel == LBM_KERNEL_AA && o.bc == LBM_BC_CAVITY && (o.world > 1 || o.local_slabs > 1) &&
         nx / (o.world * o.local_slabs) < 2)
         return fail(c, LBM_EINVAL, "kernel AA with X-slabs needs >= 2 planes per slab");
-    const int nslab_total = o.world * o.local_slabs;
+    const int nslab_total = (o.world / ry) * o.local_slabs;  // x slabs in the whole domain
     if (nx % nslab_total) return fail(c, LBM_EINVAL, "nx %d not divisible by %d slabs", nx, nslab_total);
     const int nxl = nx / nslab_total;
     if (nslab_total > 1 && nxl < 4) return fail(c, LBM_EINVAL, "slabs need >= 4 planes (got %d)", nxl);
@@ -1848,8 +1943,9 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
 
     c = new lbm_ctx();
     c->nx = nx;
-    c->ny = ny;
+    c->ny = ny / ry;  // host arrays of an X-Y rank cover its block
     c->nz = nz;
+    c->ranks_y = ry;
     c->tau = tau;
     memcpy(c->ulid, ul, sizeof ul);
     c->dt = dt;
@@ -1869,8 +1965,8 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         return st;
     };
     if (cudaSetDevice(c->device) != cudaSuccess) return bail(fail(c, LBM_ECUDA, "cudaSetDevice(%d)", c->device));
-    c->nxl_proc = nx / o.world;
-    c->x0_proc = o.rank * c->nxl_proc;
+    c->nxl_proc = nx / (o.world / ry);
+    c->x0_proc = (o.rank / ry) * c->nxl_proc;
     const int sw = o.local_slabs;
     c->yblocks = by;
     c->slabs.resize(size_t(sw) * by);  // slab j = (x range j / by, y block j % by)
@@ -1897,6 +1993,8 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         // so there it is off.  LBM_OVERLAP=0/1 forces it (A/B runs, tests).
         const char* e = getenv("LBM_OVERLAP");
         c->overlap = e ? e[0] == '1' : o.comm == LBM_COMM_NCCL;
+        // (X-Y blocks exchange their frame rows before the x spans: no split
+        // sweep, see run_steps)
         const char* f = getenv("LBM_FUSED_HALO");
         c->fused_halo = !(f && f[0] == '0');
         if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
@@ -1946,7 +2044,7 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     // free memory considered (tests).
     bool use_sc = o.kernel == LBM_KERNEL_K2_SC;
     c->peer = o.halo == LBM_HALO_PEER;
-    if (o.kernel == LBM_KERNEL_AUTO && !c->peer && by == 1) {
+    if (o.kernel == LBM_KERNEL_AUTO && !c->peer && by == 1 && ry == 1) {
         size_t freeb = 0, totalb = 0;
         if (cudaMemGetInfo(&freeb, &totalb) != cudaSuccess) {
             cudaGetLastError();
@@ -1977,16 +2075,34 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         const size_t margin = size_t(256) << 20;
         if (two + margin > freeb && one + margin <= freeb) use_sc = true;
     }
-    const int nyl = ny / by;
+    const int nyl = ny / by / ry;
+    // test knob (tests only): a periodic one-rank NCCL context exchanges its
+    // y frame rows with itself through NCCL instead of wrapping y in the
+    // kernels -- the X-Y transport on one GPU
+    const bool yself = o.comm == LBM_COMM_NCCL && o.world == 1 && o.bc == LBM_BC_PERIODIC && getenv("LBM_TEST_YSELF") &&
+                       getenv("LBM_TEST_YSELF")[0] == '1';
     for (int j = 0; j < sw * by; ++j) {
         Slab& s = c->slabs[j];
         const int bxi = j / by, byi = j % by;
-        const int grank = o.rank * sw + bxi;  // global x-slab index
+        const int grank = (o.rank / ry) * sw + bxi;  // global x-slab index
         fill_plan(nx, nyl, nz, c->esize, o.bc, grank, nslab_total, nxl, grank * nxl, &s.plan,
-                  o.kernel == LBM_KERNEL_K3 ? 3 : 2, by > 1);
+                  o.kernel == LBM_KERNEL_K3 ? 3 : 2, by > 1 || ry > 1);
         s.g.nx = nx;
         s.g.ny = nyl;
         s.y0 = byi * nyl;
+        if (ry > 1 || yself) {
+            // X-Y blocks across NCCL ranks: this rank's block, y-neighbours as ranks
+            lbm_halo_plan xy;
+            fill_plan_xy(nx, ny, nz, c->esize, o.bc, o.rank, o.world, ry, &xy);
+            s.plan.down = yself ? 0 : xy.down;
+            s.plan.up = yself ? 0 : xy.up;
+            s.plan.y0 = xy.y0;
+            s.g.ylo_wall = xy.down < 0 && o.bc == LBM_BC_CAVITY;
+            s.g.yhi_wall = xy.up < 0 && o.bc == LBM_BC_CAVITY;
+            s.g.ywrap = 0;
+            s.down = s.plan.down;
+            s.up = s.plan.up;
+        }
         if (by > 1) {
             const bool per = o.bc == LBM_BC_PERIODIC;
             s.g.ylo_wall = !per && byi == 0;
@@ -2023,9 +2139,11 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         // cavity chain: only the outer faces of the first and last slab are walls
         s.g.left_wall = (o.bc == LBM_BC_CAVITY && grank == 0);
         s.g.right_wall = (o.bc == LBM_BC_CAVITY && grank == nslab_total - 1);
-        if (o.comm == LBM_COMM_NCCL) {
-            s.left = s.plan.left;
-            s.right = s.plan.right;
+        if (o.comm == LBM_COMM_NCCL) {  // neighbour ranks (rank = x slab * ranks_y + y block)
+            s.left = s.plan.left >= 0 ? s.plan.left * ry + o.rank % ry : -1;
+            s.right = s.plan.right >= 0 ? s.plan.right * ry + o.rank % ry : -1;
+            s.plan.left = s.left;
+            s.plan.right = s.right;
         } else {
             // neighbours are local slab indices (a ring of the local slabs when
             // periodic; the same y block of the neighbouring x range)
@@ -2049,6 +2167,13 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
             // ghosts of wall sides are never read; zero everything once for determinism
             if (cudaMemset(s.buf[b], 0, bytes) != cudaSuccess) return bail(fail(c, LBM_ECUDA, "cudaMemset"));
         }
+    }
+    if (o.comm == LBM_COMM_NCCL && (c->slabs[0].down >= 0 || c->slabs[0].up >= 0)) {
+        // X-Y blocks across ranks: the four packed row-band messages
+        const Slab& s0 = c->slabs[0];
+        c->yband_bytes = size_t(s0.g.nxl) * kQ * size_t(s0.plan.y_band) * c->esize;
+        if (cudaMalloc(&c->ypack, 4 * c->yband_bytes) != cudaSuccess)
+            return bail(fail(c, LBM_ENOMEM, "cudaMalloc X-Y row bands (%zu bytes)", 4 * c->yband_bytes));
     }
     if (c->sc && cudaMalloc(&c->sc_sync, sizeof(unsigned) * (size_t(nxl) + 1)) != cudaSuccess)
         return bail(fail(c, LBM_ENOMEM, "cudaMalloc ring tickets"));
@@ -2107,6 +2232,7 @@ void lbm_destroy(lbm_ctx* c) {
         if (b) cudaFree(b);
     if (c->d_flag) cudaFree(c->d_flag);
     if (c->sc_sync) cudaFree(c->sc_sync);
+    if (c->ypack) cudaFree(c->ypack);
     if (c->stage) cudaFree(c->stage);
     if (c->comm_stream) {
         cudaStreamSynchronize(c->comm_stream);

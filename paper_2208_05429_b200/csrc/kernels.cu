@@ -127,6 +127,36 @@ cudaError_t launch_frame_fill(T* F, const SlabGeom& g, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------- X-Y row bands --
+// NCCL X-Y blocks (api.cu exchange): nbands bands of band_bytes each, at
+// stride src_stride in src and dst_stride in dst (the frame-row bands of
+// every (x, direction) plane <-> a contiguous message).  16-byte vectors:
+// bands, strides and bases are multiples of 32 B (the sector-padded rows).
+__global__ void __launch_bounds__(256) k_band_copy(const uint4* __restrict__ src, long long src_stride,
+                                                   uint4* __restrict__ dst, long long dst_stride, int band,
+                                                   int nbands) {
+    for (long long b = blockIdx.y; b < nbands; b += gridDim.y) {
+        const uint4* const sp = src + b * src_stride;
+        uint4* const dp = dst + b * dst_stride;
+        for (int e = int(blockIdx.x * blockDim.x + threadIdx.x); e < band; e += int(gridDim.x * blockDim.x))
+            dp[e] = sp[e];
+    }
+}
+
+cudaError_t launch_band_copy(const void* src, long long src_stride_bytes, void* dst, long long dst_stride_bytes,
+                             long long band_bytes, int nbands, cudaStream_t s) {
+    if (nbands <= 0 || band_bytes <= 0) return cudaSuccess;
+    if ((band_bytes | src_stride_bytes | dst_stride_bytes) % 16 || (reinterpret_cast<uintptr_t>(src) % 16) ||
+        (reinterpret_cast<uintptr_t>(dst) % 16))
+        return cudaErrorInvalidValue;
+    const int band = int(band_bytes / 16);
+    const int gx = (band + 255) / 256 < 8 ? (band + 255) / 256 : 8;
+    k_band_copy<<<dim3(unsigned(gx), unsigned(nbands < 65535 ? nbands : 65535)), 256, 0, s>>>(
+        static_cast<const uint4*>(src), src_stride_bytes / 16, static_cast<uint4*>(dst), dst_stride_bytes / 16, band,
+        nbands);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ K0 init --
 // K0a: canonical f = feq(rho, u) of every slab cell into buffer C (slot
 // layout).  rho/u are double arrays [x][y][z] / [x][y][z][3] of the slab.

@@ -46,6 +46,9 @@ bool k2_supported(const SlabGeom& g);
 // (F = cell origin); a no-op without a frame (cavity).
 template <typename T>
 cudaError_t launch_frame_fill(T* F, const SlabGeom& g, cudaStream_t s);
+// nbands bands of band_bytes, src/dst strides in bytes (NCCL X-Y row bands)
+cudaError_t launch_band_copy(const void* src, long long src_stride_bytes, void* dst, long long dst_stride_bytes,
+                             long long band_bytes, int nbands, cudaStream_t s);
 
 // K3 (k3.cu): three fused steps per HBM pass, A = f*(t-1) -> B = f*(t+2),
 // the whole slab; fp32, periodic, one slab spanning x (k3_supported).

@@ -26,7 +26,7 @@ def test_header_symbols_exported():
     for s in syms:
         assert hasattr(L, s), f"{s} declared in include/lbm.h but not exported"
     assert sorted(lbm.EXPORTS) == syms
-    assert lbm.lbm_abi_version() == 2
+    assert lbm.lbm_abi_version() == 3
 
 
 def test_library_is_sm100a():
@@ -230,3 +230,61 @@ def test_plan_rejects_bad_args():
         lbm.lbm_plan_halo(10, 4, 4, "f64", 0, 0, 3)
     with pytest.raises(lbm.LbmError):
         lbm.lbm_plan_halo(8, 4, 4, "f64", 0, 2, 2)
+
+
+def test_ranks_y_validation():
+    """NCCL X-Y blocks (lbm_opts.ranks_y): NCCL only, world and ny divisible,
+    >= 4 rows per block, the two-buffer K1/K2 storage, the NCCL exchange."""
+    o = lbm.lbm_default_opts()
+    assert o.ranks_y == 1
+    o.ranks_y = 2
+    with pytest.raises(lbm.LbmError, match="comm NCCL"):
+        lbm.lbm_create_ex(16, 16, 8, 0.6, None, "f64", o)
+    o.comm, o.nccl_id = lbm.LBM_COMM_NCCL, ctypes.cast(ctypes.create_string_buffer(128), ctypes.c_void_p)
+    o.world, o.rank, o.ranks_y = 3, 0, 2
+    with pytest.raises(lbm.LbmError, match="divisible by ranks_y"):
+        lbm.lbm_create_ex(16, 16, 8, 0.6, None, "f64", o)
+    o.world = 4
+    with pytest.raises(lbm.LbmError, match=">= 4 rows"):
+        lbm.lbm_create_ex(16, 6, 8, 0.6, None, "f64", o)
+    for k in (lbm.LBM_KERNEL_AA, lbm.LBM_KERNEL_K2_SC):
+        o.kernel = k
+        with pytest.raises(lbm.LbmError, match="K1/K2"):
+            lbm.lbm_create_ex(16, 16, 8, 0.6, None, "f64", o)
+    o.kernel, o.halo = lbm.LBM_KERNEL_AUTO, lbm.LBM_HALO_PEER
+    with pytest.raises(lbm.LbmError, match="EXCHANGE"):
+        lbm.lbm_create_ex(16, 16, 8, 0.6, None, "f64", o)
+
+
+@pytest.mark.parametrize("bc", [0, 1])
+def test_plan_halo_xy(bc):
+    """The rank grid of lbm_plan_halo_xy: rank = x slab * ranks_y + y block,
+    x neighbours in the same y block, y neighbours in the same x slab (walls
+    at the cavity ends, a ring when periodic), the frame-row bands."""
+    nx, ny, nz, world, ry = 24, 32, 12, 6, 2
+    wx = world // ry
+    for r in range(world):
+        p = lbm.lbm_plan_halo_xy(nx, ny, nz, "f64", bc, r, world, ry)
+        bx, by = divmod(r, ry)
+        assert (p.nx_local, p.x0, p.ny_local, p.y0) == (nx // wx, bx * (nx // wx), ny // ry, by * (ny // ry))
+        assert p.y_ghost == 2
+        left = (bx - 1) % wx if bc else (bx - 1 if bx > 0 else None)
+        right = (bx + 1) % wx if bc else (bx + 1 if bx < wx - 1 else None)
+        assert p.left == (-1 if left is None else left * ry + by)
+        assert p.right == (-1 if right is None else right * ry + by)
+        down = (by - 1) % ry if bc else (by - 1 if by > 0 else None)
+        up = (by + 1) % ry if bc else (by + 1 if by < ry - 1 else None)
+        assert p.down == (-1 if down is None else bx * ry + down)
+        assert p.up == (-1 if up is None else bx * ry + up)
+        nzp, nyl = p.nz_pitch, ny // ry
+        assert p.plane_q == (nyl + 4) * nzp and p.y_band == 2 * nzp
+        # rows of an (x, direction) plane: frame [0, 2), cells [2, nyl + 2), frame [nyl + 2, nyl + 4)
+        assert (p.recv_down_off, p.send_down_off) == (0, 2 * nzp)
+        assert (p.send_up_off, p.recv_up_off) == (nyl * nzp, (nyl + 2) * nzp)
+    # ranks_y = 1 is the X-slab plan
+    a = lbm.lbm_plan_halo_xy(nx, ny, nz, "f64", bc, 1, 3, 1)
+    b = lbm.lbm_plan_halo(nx, ny, nz, "f64", bc, 1, 3)
+    assert bytes(a) == bytes(b) and a.down == a.up == -1
+    for bad in ((4, 3), (6, 4)):  # world % ranks_y, ny % ranks_y (ny = 32 ok for 2) -> nx / ny checks
+        with pytest.raises(lbm.LbmError):
+            lbm.lbm_plan_halo_xy(nx, 30, nz, "f64", bc, 0, bad[0], bad[1])

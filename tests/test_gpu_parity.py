@@ -529,6 +529,45 @@ def test_nccl_transport_world1_periodic_bitwise(dtype):
     assert relerr_floor(outs[1], oracle.run(f0, lbm.LBM_BC_PERIODIC, 0.6, LID, 5)) <= TOL[dtype]
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_nccl_xy_transport_world1_bitwise(dtype, kernel, monkeypatch):
+    """The NCCL X-Y block transport (lbm_opts.ranks_y, csrc/api.cu exchange)
+    on hardware: with LBM_TEST_YSELF=1 a one-rank periodic context does not
+    wrap y in the kernels but sends its packed frame-row bands to itself
+    through ncclSend/ncclRecv (the y group), then its x spans (the x group),
+    before every K2 (and odd K1) sweep, for init, set_populations and the
+    read-backs -- bitwise equal to the in-process wrap, and to the oracle."""
+    dims = (16, 20, 36)
+    f0 = li.random_populations(57, *dims)
+    rho0 = li.uniform(58, dims[0] * dims[1] * dims[2], 0.99, 1.01).reshape(dims)
+    try:
+        lbm.lbm_nccl_unique_id()
+    except lbm.LbmError as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    outs = []
+    for yself in (False, True):
+        if yself:
+            monkeypatch.setenv("LBM_TEST_YSELF", "1")
+        kw = {"comm": lbm.LBM_COMM_NCCL, "nccl_id": lbm.lbm_nccl_unique_id()}
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=lbm.LBM_BC_PERIODIC, kernel=kernel, **kw) as lat:
+            lat.set_populations(f0)
+            lat.step(3)
+            a = lat.populations()
+            lat.step(2)
+            b = lat.populations()
+            m = lat.macroscopic()
+            lat.init_equilibrium(rho0, None)
+            lat.step(4)
+            c = lat.populations()
+            outs.append((a, b, m[0], m[1], c))
+        monkeypatch.delenv("LBM_TEST_YSELF", raising=False)
+    for x, y in zip(outs[0], outs[1]):
+        assert np.array_equal(x, y)
+    assert relerr_floor(outs[1][1], oracle.run(f0, lbm.LBM_BC_PERIODIC, 0.6, LID, 5)) <= TOL[dtype]
+
+
 # Sample boxes (origin, size) at full size: domain corners (walls, lid edge),
 # tile seams (y % 8, z % 32), x-chunk seams (x % 32) and the interior.
 def _sample_boxes(cfg):
