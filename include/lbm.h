@@ -193,8 +193,13 @@ typedef enum { LBM_HALO_AUTO = 0, LBM_HALO_EXCHANGE = 1, LBM_HALO_PEER = 2 } lbm
  * storage above).  D3Q15 and D3Q27 -- "no matter using D3Q15, D3Q19, D3Q27"
  * -- run the same method (BGK with the
  * rest-population closure, link-wise bounce-back, the moving lid, periodic
- * wrap) as one fused collide + stream step per HBM pass on one slab
- * (comm NONE, kernel AUTO or K1; EINVAL otherwise).  Host population arrays
+ * wrap) on one slab (comm NONE; kernel AUTO, K1 or K2, EINVAL otherwise):
+ * with K2 -- and AUTO, except D3Q27 fp64 where the one-step kernel is the
+ * faster -- each pair of steps is one two-step sweep per HBM pass
+ * (the paper's merge for these lattices; ECUDA under K2
+ * if the driver cannot encode TMA descriptors, AUTO then falls back), an
+ * odd remainder and kernel K1 one fused collide + stream step per pass;
+ * the results are bitwise the same.  Host population arrays
  * are f[q][nx][ny][nz] in the order lbm_lattice_table gives: i = 0 rest,
  * 1 .. (q-1)/2 the velocities whose first nonzero component is -1 (axes,
  * face diagonals, corners), then their opposites in the same order -- for

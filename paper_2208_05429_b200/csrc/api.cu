@@ -1677,6 +1677,30 @@ lbm_status dqq_set(lbm_ctx* c, const double* f) {
 template <typename T>
 lbm_status dqq_step(lbm_ctx* c, long n) {
     const T omega = T(1.0 / c->tau);
+    // pairs of steps as two-step sweeps (K2Q) with kernel K2, and with AUTO
+    // except D3Q27 fp64, whose 8x16-tile sweep (6 warps per SM, 254
+    // registers) is latency-bound and measured slower than the DRAM-bound
+    // one-step kernel (13.8k vs 14.3k MLUPS); an odd
+    // remainder (or a driver without the TMA encoder) one step at a time
+    const bool auto_k2 = !(c->dg.q == 27 && c->dt == LBM_F64);
+    for (bool k2 = c->opts.kernel == LBM_KERNEL_K2 || (c->opts.kernel == LBM_KERNEL_AUTO && auto_k2); k2 && n >= 2;
+         n -= 2) {
+        size_t slot = 0;
+        lbm_status st = prof_begin(c, slot);
+        if (st != LBM_OK) return st;
+        const cudaError_t e = launch_dqq_k2<T>(static_cast<const T*>(c->dbuf[c->dcur]),
+                                               static_cast<T*>(c->dbuf[c->dcur ^ 1]), c->dg, omega, c->ulid, c->stream);
+        if (e == cudaErrorNotSupported && c->opts.kernel == LBM_KERNEL_AUTO) {
+            cudaGetLastError();
+            break;
+        }
+        CK(e);
+        c->launches++;
+        c->k2_launches++;
+        if ((st = prof_end(c, slot, 2LL * c->dg.nx * c->dg.ny * c->dg.nz)) != LBM_OK) return st;
+        c->dcur ^= 1;
+        c->t += 2;
+    }
     for (; n > 0; --n) {
         size_t slot = 0;
         lbm_status st = prof_begin(c, slot);
@@ -1924,8 +1948,8 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     const int q = o.lattice == 0 ? 19 : o.lattice;
     if (q != 15 && q != 19 && q != 27) return fail(c, LBM_EINVAL, "bad lattice %d (15, 19 or 27)", o.lattice);
     if (q != 19 && (o.comm != LBM_COMM_NONE || o.halo != LBM_HALO_AUTO || by > 1 ||
-                    (o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K1)))
-        return fail(c, LBM_EINVAL, "lattice D3Q%d: one slab (comm NONE), kernel AUTO or K1", q);
+                    (o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K1 && o.kernel != LBM_KERNEL_K2)))
+        return fail(c, LBM_EINVAL, "lattice D3Q%d: one slab (comm NONE), kernel AUTO, K1 or K2", q);
     if (o.halo == LBM_HALO_PEER && o.comm != LBM_COMM_NCCL)
         return fail(c, LBM_EINVAL, "halo PEER needs comm NCCL (world 1: the periodic self-wrap)");
     if (o.halo == LBM_HALO_PEER && o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K2)

@@ -19,6 +19,9 @@
 // half with first nonzero component -1 -- axes, face diagonals, corners, in
 // the order below; h+1 .. 2h the opposites.  For q = 19 this is SPEC.md:109's
 // order (the D3Q19 path itself lives in d3q19.cuh / k2.cu).
+#include <cuda.h>
+
+#include <atomic>
 #include <cstdint>
 
 #include "kernels.h"
@@ -57,32 +60,98 @@ __host__ __device__ constexpr double dqq_w(int i) {
     return n == 0 ? 1.0 / 3.0 : (n == 1 ? 1.0 / 18.0 : 1.0 / 36.0);
 }
 
-// SURVEY.md 8(c) item 1 for one cell, in the oracle's operation order
+// first velocity of the half set with |c|^2 = n2, and the half set's count of them
+template <int Q>
+__host__ __device__ constexpr int dqq_rep(int n2) {
+    for (int i = 1; i <= (Q - 1) / 2; ++i)
+        if (dqq_c<Q>(i, 0) * dqq_c<Q>(i, 0) + dqq_c<Q>(i, 1) * dqq_c<Q>(i, 1) + dqq_c<Q>(i, 2) * dqq_c<Q>(i, 2) == n2)
+            return i;
+    return 0;
+}
+template <int Q>
+__host__ __device__ constexpr int dqq_count(int n2) {
+    int m = 0;
+    for (int i = 1; i <= (Q - 1) / 2; ++i)
+        if (dqq_c<Q>(i, 0) * dqq_c<Q>(i, 0) + dqq_c<Q>(i, 1) * dqq_c<Q>(i, 1) + dqq_c<Q>(i, 2) * dqq_c<Q>(i, 2) == n2)
+            ++m;
+    return m;
+}
+
+// SURVEY.md 8(c) item 1 for one cell: BGK towards feq_i = w_i rho (1 + 3 c.u
+// + 4.5 (c.u)^2 - 1.5 u.u), the rest population closing the mass.  The
+// arithmetic runs per direction pair (i, opp(i)) -- the half-sum / half-
+// difference moments, c.u without multiplications, feq_i and feq_opp from
+// one symmetric and one antisymmetric part, the rest-population closure
+// feq_0 = rho - sum_{i>0} feq_i summed in closed form per weight class (R-2,
+// as for D3Q19) -- about half
+// the FP64 operations of the oracle's term-by-term order (R-2's
+// reading for these lattices; agreement with the oracle is within the
+// tolerance, not bitwise).  K1 and K2Q both call it: they agree bit for bit.
 template <typename T, int Q>
 __device__ __forceinline__ void dqq_collide(T (&f)[Q], T omega) {
-    T r = T(0), jx = T(0), jy = T(0), jz = T(0);
-    static_for<0, Q>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
-        r = r + f[i];
-        jx = jx + T(dqq_c<Q>(i, 0)) * f[i];
-        jy = jy + T(dqq_c<Q>(i, 1)) * f[i];
-        jz = jz + T(dqq_c<Q>(i, 2)) * f[i];
+    constexpr int H = (Q - 1) / 2;
+    T sm[H], df[H];
+    static_for<0, H>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        sm[j] = f[1 + j] + f[1 + j + H];
+        df[j] = f[1 + j] - f[1 + j + H];
     });
-    const T ux = jx / r, uy = jy / r, uz = jz / r;
-    const T usq = ux * ux + uy * uy + uz * uz;
-    T feq[Q];
-    T rest = r;
-    static_for<1, Q>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
-        const T cu = T(dqq_c<Q>(i, 0)) * ux + T(dqq_c<Q>(i, 1)) * uy + T(dqq_c<Q>(i, 2)) * uz;
-        feq[i] = T(dqq_w<Q>(i)) * r * (T(1) + T(3) * cu + T(4.5) * cu * cu - T(1.5) * usq);
-        rest = rest - feq[i];
+    T r = f[0];
+    static_for<0, H>([&](auto jc) { r = r + sm[decltype(jc)::value]; });
+    // j_a = sum over the half set of c_a (f_i - f_opp)
+    T jm[3];
+    static_for<0, 3>([&](auto ac) {
+        constexpr int ax = decltype(ac)::value;
+        bool first = true;
+        T acc = T(0);
+        static_for<0, H>([&](auto jc) {
+            constexpr int j = decltype(jc)::value;
+            constexpr int cc = dqq_c<Q>(1 + j, ax);
+            if constexpr (cc != 0) {
+                const T v = cc > 0 ? df[j] : -df[j];
+                acc = first ? v : acc + v;
+                first = false;
+            }
+        });
+        jm[ax] = acc;
     });
-    feq[0] = rest;
-    static_for<0, Q>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
-        f[i] = f[i] - omega * (f[i] - feq[i]);
+    const T rinv = rcp_nr<T>(r);
+    const T ux = jm[0] * rinv, uy = jm[1] * rinv, uz = jm[2] * rinv;
+    const T usq = fma(ux, ux, fma(uy, uy, uz * uz));
+    const T base = fma(T(-1.5), usq, T(1));
+    const T om1 = T(1) - omega;
+    static_for<0, H>([&](auto jc) {
+        constexpr int j = decltype(jc)::value, i = 1 + j;
+        constexpr int cx = dqq_c<Q>(i, 0), cy = dqq_c<Q>(i, 1), cz = dqq_c<Q>(i, 2);
+        T cu;
+        if constexpr (cx != 0) {
+            cu = cx > 0 ? ux : -ux;
+            if constexpr (cy != 0) cu = cy > 0 ? cu + uy : cu - uy;
+            if constexpr (cz != 0) cu = cz > 0 ? cu + uz : cu - uz;
+        } else if constexpr (cy != 0) {
+            cu = cy > 0 ? uy : -uy;
+            if constexpr (cz != 0) cu = cz > 0 ? cu + uz : cu - uz;
+        } else {
+            cu = cz > 0 ? uz : -uz;
+        }
+        const T owr = omega * (T(dqq_w<Q>(i)) * r);      // omega w_i rho (one per weight class)
+        const T sym = owr * fma(T(4.5) * cu, cu, base);  // omega (feq_i + feq_opp) / 2
+        const T asym = (T(3) * owr) * cu;                // omega (feq_i - feq_opp) / 2
+        f[i] = fma(om1, f[i], sym + asym);
+        f[i + H] = fma(om1, f[i + H], sym - asym);
     });
+    // closure: sum_{i>0} feq_i = 2 sum over weight classes c of
+    // w_c rho (n_c (1 - 1.5 u.u) + 4.5 k_c u.u), n_c half-set vectors of class
+    // c and sum_{half set of c} (c.u)^2 = k_c u.u (axes 1, face diagonals 4,
+    // corners 4), with the same rounded w_c rho as the populations, so the
+    // weights' rounding cancels in the mass (R-2)
+    T clos = T(0);
+    static_for<1, 4>([&](auto nc) {
+        constexpr int n2 = decltype(nc)::value;  // |c|^2 of the class
+        constexpr int rep = dqq_rep<Q>(n2), cnt = dqq_count<Q>(n2), kc = n2 == 1 ? 1 : 4;
+        if constexpr (cnt > 0) clos = clos + (T(dqq_w<Q>(rep)) * r) * fma(T(4.5 * kc), usq, T(cnt) * base);
+    });
+    f[0] = fma(om1, f[0], omega * (r - T(2) * clos));
 }
 
 }  // namespace
@@ -213,6 +282,283 @@ __global__ void __launch_bounds__(256) k_dqq_import(const double* __restrict__ s
     });
 }
 
+
+// ------------------------------------------------------------------ K2Q --
+// Two collide + push steps per HBM pass for D3Q15 / D3Q27 (the paper's
+// two-step merge, which it states for any of these
+// lattices).  K2 (k2.cu) reorganised for push-form canonical
+// storage: each CTA owns a TY x TZ output tile and marches along x over a
+// chunk of planes.  Per input plane p:
+//   1. TMA stages f(t) of the tile plus a one-cell halo (T+1): one box per
+//      direction, all at the same origin (push form: a cell reads its own
+//      populations), double-buffered on one mbarrier.  Cells beyond a cavity
+//      wall are zero-filled and never collide; a periodic box's halo cells
+//      beyond the domain reload their wrapped cell from global memory.
+//   2. Step 1: every cell of T+1 collides (dqq_collide) and pushes f*_i into
+//      a destination-indexed SMEM ring at x + c_i when that lies in the tile;
+//      a tile cell whose link leaves the domain bounces f*_i (+ lid) into its
+//      own slot opp(i) -- so the ring holds exactly f(t+1) of the tile.
+//   3. Step 2 of plane p-2 (complete since this iteration's barrier): collide
+//      and push f*(t+1) to B at x + c_i (or bounce into the own slot), every
+//      destination slot written exactly once, as in k_dqq_step.
+// Same collision and wall arithmetic as k_dqq_step, so K2Q == step o step
+// bit for bit (tests/test_gpu_dqq.py).  Ring depths per c_x group: M (c_x =
+// -1) 3 destination planes (p-2 read, p-1 pushed, p bounced), Z 3, P 4.
+namespace {
+
+template <int Q>
+__host__ __device__ constexpr int kq_grp(int i) { return dqq_c<Q>(i, 0) + 1; }  // 0: c_x = -1, 1: 0, 2: +1
+template <int Q>
+__host__ __device__ constexpr int kq_gidx(int i) {  // index of i within its c_x group
+    int m = 0;
+    for (int j = 0; j < i; ++j)
+        if (dqq_c<Q>(j, 0) == dqq_c<Q>(i, 0)) ++m;
+    return m;
+}
+template <int Q>
+__host__ __device__ constexpr int kq_gsize(int gg) {
+    int m = 0;
+    for (int j = 0; j < Q; ++j)
+        if (dqq_c<Q>(j, 0) + 1 == gg) ++m;
+    return m;
+}
+__host__ __device__ constexpr int kq_round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+template <typename T, int Q, int TY_, int TZ_>
+struct KQCfg {
+    static constexpr int TY = TY_, TZ = TZ_, HY = TY + 2, HZ = TZ + 2;
+    static constexpr int ZPAD = 16 / int(sizeof(T));  // TMA: 16 B aligned innermost origin
+    static constexpr int BW = TZ + 2 * ZPAD, BOX = HY * BW;
+    static constexpr int BOXE = kq_round_up(BOX * int(sizeof(T)), 128) / int(sizeof(T));
+    static constexpr int NT = kq_round_up(HY * HZ, 32);
+    static constexpr int RP = TY * TZ;
+    static constexpr int GM = kq_gsize<Q>(0), GZ = kq_gsize<Q>(1), GP = kq_gsize<Q>(2);
+    static constexpr int DM = 3, DZ = 3, DP = 4;
+    static constexpr int RING = (DM * GM + DZ * GZ + DP * GP) * RP;
+    static constexpr size_t SMEM = size_t(2 * Q * BOXE + RING) * sizeof(T) + 2 * sizeof(uint64_t);
+    static constexpr uint32_t TX = uint32_t(Q * BOX * sizeof(T));
+};
+
+__device__ __forceinline__ uint32_t kq_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ bool kq_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(kq_smem(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void kq_wait(uint64_t* bar, uint32_t parity) {
+    for (uint32_t spin = 0; !kq_try_wait(bar, parity); ++spin)
+        if (spin > (1u << 28)) __trap();  // a TMA that never lands: a kernel error, not a hang
+}
+__device__ __forceinline__ int kq_wrap(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
+
+}  // namespace
+
+template <typename T, int Q, int BC, int TY, int TZ>
+__global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ>::NT, 1)
+    k_dqq_k2(const __grid_constant__ CUtensorMap tm, const T* __restrict__ A, T* __restrict__ B, DqqGeom g, T omega,
+             double ulx, double uly, int chunk) {
+    using C = KQCfg<T, Q, TY, TZ>;
+    constexpr bool PER = BC == BC_PERIODIC;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* const stage = reinterpret_cast<T*>(smem_raw);
+    T* const ringM = stage + 2 * Q * C::BOXE;
+    T* const ringZ = ringM + C::DM * C::GM * C::RP;
+    T* const ringP = ringZ + C::DZ * C::GZ * C::RP;
+    uint64_t* const bar = reinterpret_cast<uint64_t*>(ringP + C::DP * C::GP * C::RP);
+
+    const int ntz = (g.nz + TZ - 1) / TZ;
+    const int z0 = int(blockIdx.x % ntz) * TZ, y0 = int(blockIdx.x / ntz) * TY;  // z-fastest tile order
+    const int xs = int(blockIdx.y) * chunk, xe = min(xs + chunk, g.nx);
+    const int p_first = PER ? xs - 1 : max(xs - 1, 0), p_last = PER ? xe : min(xe, g.nx - 1);
+    const long long plane = (long long)g.ny * g.nzp;
+
+    // step-1 cell (box coordinates a, b; cell qy, qz): interior columns row by
+    // row, then the two halo columns (K2's mapping)
+    const int tid = threadIdx.x;
+    int a, b;
+    if (tid < C::HY * TZ) {
+        a = tid / TZ;
+        b = 1 + tid % TZ;
+    } else {
+        const int j = tid - C::HY * TZ;
+        a = j >> 1;
+        b = (j & 1) ? TZ + 1 : 0;
+    }
+    const bool act1 = tid < C::HY * C::HZ;
+    const int qy = y0 - 1 + a, qz = z0 - 1 + b;
+    const bool q_in = act1 && (PER ? (qy >= -1 && qy <= g.ny && qz >= -1 && qz <= g.nz)
+                                   : (qy >= 0 && qy < g.ny && qz >= 0 && qz < g.nz));
+    const bool q_wrap = PER && q_in && (qy < 0 || qy >= g.ny || qz < 0 || qz >= g.nz);
+    const bool q_tile = act1 && a >= 1 && a <= TY && b >= 1 && b <= TZ;
+    const int soff = a * C::BW + b + C::ZPAD - 1;  // staged entry of (a, b)
+    const int toff = (a - 1) * TZ + (b - 1);        // ring entry of (a, b) (tile coordinates)
+    const bool rowok[3] = {a >= 2 && a <= TY + 1, a >= 1 && a <= TY, a <= TY - 1};
+    const bool colok[3] = {b >= 2 && b <= TZ + 1, b >= 1 && b <= TZ, b <= TZ - 1};
+    // cavity walls of the step-1 cell (y, z; x per plane)
+    const bool wyl = !PER && qy == 0, wyh = !PER && qy == g.ny - 1, wzl = !PER && qz == 0, wzh = !PER && qz == g.nz - 1;
+    // step-2 cell
+    const int y2 = tid / TZ, z2 = tid % TZ, yy = y0 + y2, zz = z0 + z2;
+    const bool in2 = tid < TY * TZ && yy < g.ny && zz < g.nz;
+    const bool warp2 = (tid & ~31) < TY * TZ;
+    const bool vyl = !PER && yy == 0, vyh = !PER && yy == g.ny - 1, vzl = !PER && zz == 0, vzh = !PER && zz == g.nz - 1;
+    // periodic destination offsets of the step-2 cell per c_y, c_z
+    const long long yo[3] = {(long long)kq_wrap(yy - 1, g.ny) * g.nzp, (long long)yy * g.nzp,
+                             (long long)kq_wrap(yy + 1, g.ny) * g.nzp};
+    const int zo[3] = {kq_wrap(zz - 1, g.nz), zz, kq_wrap(zz + 1, g.nz)};
+
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    auto issue = [&](int p, int s) {  // one thread: stage plane p into buffer s
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(kq_smem(&bar[s])), "r"(C::TX)
+                     : "memory");
+        const int px = PER ? kq_wrap(p, g.nx) : p;
+        static_for<0, Q>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(kq_smem(stage + (s * Q + k) * C::BOXE)),
+                "l"(reinterpret_cast<uint64_t>(&tm)), "r"(z0 - C::ZPAD), "r"(y0 - 1), "r"(px), "r"(k),
+                "r"(kq_smem(&bar[s])), "l"(pol)
+                : "memory");
+        });
+    };
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(kq_smem(&bar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(kq_smem(&bar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (p_first <= p_last) issue(p_first, 0);
+        if (p_first + 1 <= p_last) issue(p_first + 1, 1);
+    }
+    // ring plane of group G for destination plane dp (dp >= -2)
+    auto ring = [&](auto G, int dp) -> T* {
+        constexpr int gg = decltype(G)::value;
+        if constexpr (gg == 0) return ringM + ((dp + 6) % 3) * C::GM * C::RP;
+        else if constexpr (gg == 1) return ringZ + ((dp + 6) % 3) * C::GZ * C::RP;
+        else return ringP + ((dp + 8) & 3) * C::GP * C::RP;
+    };
+
+    for (int p = xs - 1; p <= xe + 1; ++p) {
+        const bool has1 = p >= p_first && p <= p_last;
+        const int c = p - p_first, s = c & 1;
+        T fs[Q];
+        if (has1) {
+            kq_wait(&bar[s], uint32_t(c >> 1) & 1u);
+            const T* const sp = stage + s * Q * C::BOXE + (act1 ? soff : C::ZPAD);
+            static_for<0, Q>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                fs[k] = sp[k * C::BOXE];
+            });
+            if (q_wrap) {  // periodic halo cell beyond the domain: its wrapped cell
+                const long long o = (long long)kq_wrap(p, g.nx) * plane + (long long)kq_wrap(qy, g.ny) * g.nzp +
+                                    kq_wrap(qz, g.nz);
+                static_for<0, Q>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    fs[k] = A[(long long)k * g.pq + o];
+                });
+            }
+        }
+        __syncthreads();  // stage of plane p consumed, ring of destination p-2 complete
+        if (tid == 0 && has1 && p + 2 <= p_last) issue(p + 2, s);
+
+        // ---- step 2 of plane d = p - 2 and step 1 of plane p ----
+        const int d = p - 2;
+        const bool do2 = d >= xs && warp2;
+        T f2[Q];
+        if (do2) {
+            const int t = in2 ? y2 * TZ + z2 : 0;
+            static_for<0, Q>([&](auto kc) {
+                constexpr int i = decltype(kc)::value;
+                f2[i] = ring(std::integral_constant<int, kq_grp<Q>(i)>{}, d)[kq_gidx<Q>(i) * C::RP + t];
+            });
+        }
+        if (do2) dqq_collide<T, Q>(f2, omega);
+        if (has1) dqq_collide<T, Q>(fs, omega);
+        if (do2 && in2) {
+            const long long own = (long long)d * plane + (long long)yy * g.nzp + zz;
+            const bool vxl = !PER && d == 0, vxh = !PER && d == g.nx - 1;
+            const long long xo[3] = {(long long)kq_wrap(d - 1, g.nx) * plane, (long long)d * plane,
+                                     (long long)kq_wrap(d + 1, g.nx) * plane};
+            static_for<0, Q>([&](auto kc) {
+                constexpr int i = decltype(kc)::value;
+                constexpr int cx = dqq_c<Q>(i, 0), cy = dqq_c<Q>(i, 1), cz = dqq_c<Q>(i, 2);
+                if constexpr (PER) {
+                    __stcs(B + (long long)i * g.pq + xo[cx + 1] + yo[cy + 1] + zo[cz + 1], f2[i]);
+                } else {
+                    bool out = false;
+                    if constexpr (cx == -1) out = out || vxl;
+                    if constexpr (cx == 1) out = out || vxh;
+                    if constexpr (cy == -1) out = out || vyl;
+                    if constexpr (cy == 1) out = out || vyh;
+                    if constexpr (cz == -1) out = out || vzl;
+                    if constexpr (cz == 1) out = out || vzh;
+                    if (!out) {
+                        __stcs(B + (long long)i * g.pq + own + (long long)cx * plane + cy * g.nzp + cz, f2[i]);
+                    } else {
+                        constexpr int o = dqq_opp<Q>(i);
+                        T v = f2[i];
+                        if constexpr (cz == 1) {
+                            if (vzh) {  // the moving lid: 6 w_o rho_w (c_o . u_lid), rho_w = 1
+                                const double cu = dqq_c<Q>(o, 0) * ulx + dqq_c<Q>(o, 1) * uly;
+                                v = v + T(6.0 * dqq_w<Q>(o) * 1.0 * cu);
+                            }
+                        }
+                        __stcs(B + (long long)o * g.pq + own, v);
+                    }
+                }
+            });
+        }
+        if (has1 && q_in) {
+            // pushes into the tile: direction i streams to (p + c_x, a - 1 + c_y, b - 1 + c_z)
+            static_for<0, Q>([&](auto kc) {
+                constexpr int i = decltype(kc)::value;
+                constexpr int cx = dqq_c<Q>(i, 0), cy = dqq_c<Q>(i, 1), cz = dqq_c<Q>(i, 2);
+                if (rowok[cy + 1] && colok[cz + 1])
+                    ring(std::integral_constant<int, kq_grp<Q>(i)>{}, p + cx)[kq_gidx<Q>(i) * C::RP + toff + cy * TZ + cz] =
+                        fs[i];
+            });
+            if constexpr (!PER) {
+                // links of a tile cell that leave the domain: bounce-back (+ lid) into its own slot
+                if (q_tile) {
+                    const bool wxl = p == 0, wxh = p == g.nx - 1;
+                    static_for<0, Q>([&](auto kc) {
+                        constexpr int i = decltype(kc)::value;
+                        constexpr int cx = dqq_c<Q>(i, 0), cy = dqq_c<Q>(i, 1), cz = dqq_c<Q>(i, 2);
+                        bool out = false;
+                        if constexpr (cx == -1) out = out || wxl;
+                        if constexpr (cx == 1) out = out || wxh;
+                        if constexpr (cy == -1) out = out || wyl;
+                        if constexpr (cy == 1) out = out || wyh;
+                        if constexpr (cz == -1) out = out || wzl;
+                        if constexpr (cz == 1) out = out || wzh;
+                        if (out) {
+                            constexpr int o = dqq_opp<Q>(i);
+                            T v = fs[i];
+                            if constexpr (cz == 1) {
+                                if (wzh) {
+                                    const double cu = dqq_c<Q>(o, 0) * ulx + dqq_c<Q>(o, 1) * uly;
+                                    v = v + T(6.0 * dqq_w<Q>(o) * 1.0 * cu);
+                                }
+                            }
+                            ring(std::integral_constant<int, kq_grp<Q>(o)>{}, p)[kq_gidx<Q>(o) * C::RP + toff] = v;
+                        }
+                    });
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ host --
 namespace {
 dim3 dqq_grid(int nz, int ny, int nx) { return dim3((nz + 31) / 32, (ny + 7) / 8, nx); }
@@ -276,6 +622,88 @@ cudaError_t launch_dqq_import(const double* src, T* A, const DqqGeom& g, int xbe
 }
 #undef LBM_DQQ_DISPATCH
 
+
+namespace {
+
+using KqEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <typename T, int Q, int BC, int TY, int TZ>
+cudaError_t launch_kq(const T* A, T* B, const DqqGeom& g, T omega, const double ulid[3], cudaStream_t s) {
+    using C = KQCfg<T, Q, TY, TZ>;
+    static_assert(C::SMEM <= 227 * 1024, "K2Q tile does not fit shared memory");
+    auto kern = k_dqq_k2<T, Q, BC, TY, TZ>;
+    // the large-shared-memory opt-in is per device (context): once per ordinal
+    static std::atomic<int> done[64];
+    const int dev = device_ordinal();
+    if (!done[dev].load(std::memory_order_acquire)) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+        if (e != cudaSuccess) return e;
+        done[dev].store(1, std::memory_order_release);
+    }
+    auto enc = reinterpret_cast<KqEncodeFn>(tma_encode_entry());
+    if (!enc) return cudaErrorNotSupported;
+    // canonical [q][x][y][z] as a 4D tensor (z, y, x, q); cells beyond the
+    // domain read as zero
+    CUtensorMap map;
+    const cuuint64_t dims[4] = {cuuint64_t(g.nz), cuuint64_t(g.ny), cuuint64_t(g.nx), cuuint64_t(Q)};
+    const cuuint64_t strides[3] = {cuuint64_t(g.nzp) * sizeof(T), cuuint64_t(g.ny) * g.nzp * sizeof(T),
+                                   cuuint64_t(g.pq) * sizeof(T)};
+    const cuuint32_t box[4] = {cuuint32_t(C::BW), cuuint32_t(C::HY), 1u, 1u};
+    const cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    if (enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+            const_cast<T*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_64B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    // x chunks of <= 32 planes (K2's short-chunk rule: co-resident tiles stay
+    // within a few planes, so halo rows re-staged by a neighbour hit L2),
+    // filling whole waves of one CTA per SM; each chunk re-computes ~2.5
+    // step-1 planes and ~2 planes of pipeline fill
+    const long long ntiles = (long long)((g.ny + TY - 1) / TY) * ((g.nz + TZ - 1) / TZ);
+    const long long slots = device_sm_count();
+    int best = 1;
+    double best_cost = 1e300;
+    for (int nch = 1; nch <= g.nx; ++nch) {
+        const int ch = (g.nx + nch - 1) / nch;
+        if (ch > 32 && nch < g.nx) continue;
+        const double waves = double((ntiles * ((g.nx + ch - 1) / ch) + slots - 1) / slots);
+        const double cost = waves * (double(g.nx) / nch + 4.5);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = nch;
+        }
+        if (ch <= 8) break;
+    }
+    const int chunk = (g.nx + best - 1) / best;
+    const dim3 grid(unsigned(ntiles), unsigned((g.nx + chunk - 1) / chunk));
+    kern<<<grid, C::NT, C::SMEM, s>>>(map, A, B, g, omega, ulid[0], ulid[1], chunk);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// Tiles (the largest whose stage + ring fit 227 KB): D3Q27 fp64 8x16 (178
+// KB), fp32 8x32 (178 KB); D3Q15 fp64 8x32 (184 KB), fp32 16x32 (184 KB).
+template <typename T>
+cudaError_t launch_dqq_k2(const T* A, T* B, const DqqGeom& g, T omega, const double ulid[3], cudaStream_t s) {
+    if (!tma_encode_entry()) return cudaErrorNotSupported;
+    if (g.nx < 1 || (g.nzp * sizeof(T)) % 16) return cudaErrorInvalidValue;
+    constexpr bool F64 = sizeof(T) == 8;
+    constexpr int TY27 = 8, TZ27 = F64 ? 16 : 32, TY15 = F64 ? 8 : 16, TZ15 = 32;
+    const bool per = g.bc == BC_PERIODIC;
+    switch (g.q) {
+        case 27:
+            return per ? launch_kq<T, 27, BC_PERIODIC, TY27, TZ27>(A, B, g, omega, ulid, s)
+                       : launch_kq<T, 27, BC_CAVITY, TY27, TZ27>(A, B, g, omega, ulid, s);
+        case 15:
+            return per ? launch_kq<T, 15, BC_PERIODIC, TY15, TZ15>(A, B, g, omega, ulid, s)
+                       : launch_kq<T, 15, BC_CAVITY, TY15, TZ15>(A, B, g, omega, ulid, s);
+        default:
+            return cudaErrorInvalidValue;
+    }
+}
+
 void dqq_table(int q, int* c, double* w) {
     for (int i = 0; i < q; ++i) {
         for (int a = 0; a < 3; ++a) c[3 * i + a] = q == 15 ? dqq_c<15>(i, a) : (q == 27 ? dqq_c<27>(i, a) : 0);
@@ -290,7 +718,8 @@ void dqq_table(int q, int* c, double* w) {
                                                cudaStream_t);                                                  \
     template cudaError_t launch_dqq_box<T>(const T*, const DqqGeom&, int, int, int, int, int, int, double*,    \
                                            cudaStream_t);                                                      \
-    template cudaError_t launch_dqq_import<T>(const double*, T*, const DqqGeom&, int, int, cudaStream_t);
+    template cudaError_t launch_dqq_import<T>(const double*, T*, const DqqGeom&, int, int, cudaStream_t);     \
+    template cudaError_t launch_dqq_k2<T>(const T*, T*, const DqqGeom&, T, const double*, cudaStream_t);
 LBM_DQQ_INST(double)
 LBM_DQQ_INST(float)
 #undef LBM_DQQ_INST

@@ -802,6 +802,11 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
 
 }  // namespace
 
+// shared with the other lattices' two-step sweep (dqq.cu)
+void* tma_encode_entry() { return reinterpret_cast<void*>(get_encode()); }
+int device_sm_count() { return num_sms(); }
+int device_ordinal() { return current_device(); }
+
 template <typename T>
 bool k2_supported(const SlabGeom& g) {
     if (!get_encode()) return false;

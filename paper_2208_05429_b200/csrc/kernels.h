@@ -76,6 +76,17 @@ cudaError_t launch_dqq_box(const T* A, const DqqGeom& g, int x0, int y0, int z0,
 template <typename T>
 cudaError_t launch_dqq_import(const double* src, T* A, const DqqGeom& g, int xbeg, int nxc, cudaStream_t s);
 void dqq_table(int q, int* c, double* w);
+// Two fused collide + push steps per HBM pass (K2Q, dqq.cu): canonical
+// A = f(t) -> B = f(t+2), the whole lattice.  cudaErrorNotSupported when the
+// driver has no TMA descriptor encoder.
+template <typename T>
+cudaError_t launch_dqq_k2(const T* A, T* B, const DqqGeom& g, T omega, const double ulid[3], cudaStream_t s);
+
+// k2.cu helpers shared with dqq.cu: cuTensorMapEncodeTiled (null if the
+// driver lacks it), the current device's SM count and ordinal
+void* tma_encode_entry();
+int device_sm_count();
+int device_ordinal();
 
 // canonical feq of planes [xbeg, xbeg + nxc) (nxc < 0: the whole slab); rho/u
 // point at the first of those planes

@@ -132,7 +132,7 @@ def test_lattice_validation():
     with pytest.raises(lbm.LbmError, match="D3Q27"):
         lbm.lbm_create_ex(8, 8, 8, 0.6, None, "f64", o)
     o = lbm.lbm_default_opts()
-    o.lattice, o.kernel = 15, lbm.LBM_KERNEL_K2
+    o.lattice, o.kernel = 15, lbm.LBM_KERNEL_AA
     with pytest.raises(lbm.LbmError, match="D3Q15"):
         lbm.lbm_create_ex(8, 8, 8, 0.6, None, "f64", o)
     with pytest.raises(lbm.LbmError):

@@ -68,3 +68,46 @@ def test_lid_cavity_recipe(q, dtype):
     u_ref = np.einsum("ia,ixyz->xyza", c.astype(float), ref) / r_ref[..., None]
     assert np.max(np.abs(r - r_ref)) <= 10 * TOL[dtype] and np.max(np.abs(u - u_ref)) <= 10 * TOL[dtype]
     assert abs(math.fsum(got.ravel()) - m0) / m0 <= (1e-13 if dtype == "f64" else 1e-6)
+
+
+@pytest.mark.parametrize("q", [15, 27])
+@pytest.mark.parametrize("dims", [(70, 21, 45), (3, 5, 7), (33, 9, 100), (2, 17, 33), (6, 40, 64)])
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_CAVITY, lbm.LBM_BC_PERIODIC])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_two_step_sweep_bitwise(q, dims, bc, dtype):
+    """K2Q (two collide + push steps per HBM pass, the paper's merge for these
+    lattices) equals two one-step launches bit for
+    bit: ragged tiles in y and z, several x chunks, one-plane and one-row
+    lattices, walls and wraps, odd step counts (a one-step remainder)."""
+    f0 = li.uniform(90 + q, q * int(np.prod(dims)), 0.01, 0.06).reshape(q, *dims)
+    outs = []
+    for kern in (lbm.LBM_KERNEL_K1, lbm.LBM_KERNEL_K2):
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=bc, lattice=q, kernel=kern) as lat:
+            lat.set_populations(f0)
+            lat.step(4)
+            a = lat.populations()
+            lat.step(3)
+            outs.append((a, lat.populations(), lbm.lbm_get_stats(lat.ctx).k2_launches))
+    assert outs[0][2] == 0 and outs[1][2] == 3
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("q", [15, 27])
+def test_two_step_sweep_cavity_vs_oracle(q):
+    """A 40 x 24 x 48 lid cavity (several tiles and x chunks) in fp64 through
+    K2Q sweeps against the oracle after 10 steps, element by element; AUTO
+    takes them too, except for D3Q27 fp64 (one-step kernel: faster there)."""
+    dims = (40, 24, 48)
+    rho = 1.0 + li.uniform(5, int(np.prod(dims)), -1e-3, 1e-3).reshape(dims)
+    ref = oracle.dqq_run(q, oracle.dqq_init_equilibrium(q, *dims, rho), lbm.LBM_BC_CAVITY, 0.6, LID, 10)
+    with lbm.Lattice(*dims, 0.6, LID, "f64", lattice=q, kernel=lbm.LBM_KERNEL_K2) as lat:
+        lat.init_equilibrium(rho, None)
+        lat.step(10)
+        got = lat.populations()
+        assert lbm.lbm_get_stats(lat.ctx).k2_launches == 5
+    assert float(np.max(np.abs(got - ref) / np.abs(ref))) <= TOL["f64"]
+    with lbm.Lattice(*dims, 0.6, LID, "f64", lattice=q) as lat:
+        lat.init_equilibrium(rho, None)
+        lat.step(10)
+        assert lbm.lbm_get_stats(lat.ctx).k2_launches == (0 if q == 27 else 5)
+        assert np.array_equal(lat.populations(), got)
