@@ -93,20 +93,22 @@ def test_two_step_sweep_bitwise(q, dims, bc, dtype):
 
 
 @pytest.mark.parametrize("q", [15, 27])
-def test_two_step_sweep_cavity_vs_oracle(q):
+@pytest.mark.parametrize("tau,lid", [(0.6, LID), (0.9, (0.03, -0.02, 0.0)), (0.51, (0.0, 0.04, 0.0))])
+def test_two_step_sweep_cavity_vs_oracle(q, tau, lid):
     """A 40 x 24 x 48 lid cavity (several tiles and x chunks) in fp64 through
-    K2Q sweeps against the oracle after 10 steps, element by element; AUTO
+    K2Q sweeps against the oracle after 10 steps, element by element, for
+    three relaxation times and lids along x, y and the xy diagonal; AUTO
     takes them too, except for D3Q27 fp64 (one-step kernel: faster there)."""
     dims = (40, 24, 48)
     rho = 1.0 + li.uniform(5, int(np.prod(dims)), -1e-3, 1e-3).reshape(dims)
-    ref = oracle.dqq_run(q, oracle.dqq_init_equilibrium(q, *dims, rho), lbm.LBM_BC_CAVITY, 0.6, LID, 10)
-    with lbm.Lattice(*dims, 0.6, LID, "f64", lattice=q, kernel=lbm.LBM_KERNEL_K2) as lat:
+    ref = oracle.dqq_run(q, oracle.dqq_init_equilibrium(q, *dims, rho), lbm.LBM_BC_CAVITY, tau, lid, 10)
+    with lbm.Lattice(*dims, tau, lid, "f64", lattice=q, kernel=lbm.LBM_KERNEL_K2) as lat:
         lat.init_equilibrium(rho, None)
         lat.step(10)
         got = lat.populations()
         assert lbm.lbm_get_stats(lat.ctx).k2_launches == 5
     assert float(np.max(np.abs(got - ref) / np.abs(ref))) <= TOL["f64"]
-    with lbm.Lattice(*dims, 0.6, LID, "f64", lattice=q) as lat:
+    with lbm.Lattice(*dims, tau, lid, "f64", lattice=q) as lat:
         lat.init_equilibrium(rho, None)
         lat.step(10)
         assert lbm.lbm_get_stats(lat.ctx).k2_launches == (0 if q == 27 else 5)
