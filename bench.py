@@ -357,7 +357,7 @@ def main():
     # roofline.traffic: measured DRAM bytes per sweep launch from the newest
     # committed ncu capture of this workload/dtype/kernel (profiles/rNN_traffic.json)
     traffic = None
-    for tf in ("r02b_traffic.json", "r02_traffic.json", "r01_traffic.json"):
+    for tf in ("r02c_traffic.json", "r02b_traffic.json", "r02_traffic.json", "r01_traffic.json"):
         try:
             tj = json.load(open(os.path.join(ROOT, "profiles", tf)))
             t = tj.get(cfg.name, {}).get(dominant, {}).get(args.dtype) if world == 1 else None
