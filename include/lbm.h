@@ -194,8 +194,7 @@ typedef enum { LBM_HALO_AUTO = 0, LBM_HALO_EXCHANGE = 1, LBM_HALO_PEER = 2 } lbm
  * -- run the same method (BGK with the
  * rest-population closure, link-wise bounce-back, the moving lid, periodic
  * wrap) on one slab (comm NONE; kernel AUTO, K1 or K2, EINVAL otherwise):
- * with K2 -- and AUTO, except D3Q27 fp64 where the one-step kernel is the
- * faster -- each pair of steps is one two-step sweep per HBM pass
+ * with AUTO or K2 each pair of steps is one two-step sweep per HBM pass
  * (the paper's merge for these lattices; ECUDA under K2
  * if the driver cannot encode TMA descriptors, AUTO then falls back), an
  * odd remainder and kernel K1 one fused collide + stream step per pass;

@@ -1677,14 +1677,11 @@ lbm_status dqq_set(lbm_ctx* c, const double* f) {
 template <typename T>
 lbm_status dqq_step(lbm_ctx* c, long n) {
     const T omega = T(1.0 / c->tau);
-    // pairs of steps as two-step sweeps (K2Q) with kernel K2, and with AUTO
-    // except D3Q27 fp64, whose 8x16-tile sweep (6 warps per SM, 254
-    // registers) is latency-bound and measured slower than the DRAM-bound
-    // one-step kernel (13.8k vs 14.3k MLUPS); an odd
-    // remainder (or a driver without the TMA encoder) one step at a time
-    const bool auto_k2 = !(c->dg.q == 27 && c->dt == LBM_F64);
-    for (bool k2 = c->opts.kernel == LBM_KERNEL_K2 || (c->opts.kernel == LBM_KERNEL_AUTO && auto_k2); k2 && n >= 2;
-         n -= 2) {
+    // pairs of steps as two-step sweeps (K2Q) unless kernel K1 was chosen
+    // (measured faster than the one-step kernel for every lattice and dtype,
+    // DESIGN.md section 11); an odd remainder (or, under AUTO, a driver
+    // without the TMA encoder) one step at a time
+    for (bool k2 = c->opts.kernel != LBM_KERNEL_K1; k2 && n >= 2; n -= 2) {
         size_t slot = 0;
         lbm_status st = prof_begin(c, slot);
         if (st != LBM_OK) return st;

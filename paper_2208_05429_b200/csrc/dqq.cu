@@ -324,13 +324,17 @@ __host__ __device__ constexpr int kq_gsize(int gg) {
 }
 __host__ __device__ constexpr int kq_round_up(int v, int m) { return (v + m - 1) / m * m; }
 
-template <typename T, int Q, int TY_, int TZ_>
+template <typename T, int Q, int TY_, int TZ_, bool WS_ = false>
 struct KQCfg {
     static constexpr int TY = TY_, TZ = TZ_, HY = TY + 2, HZ = TZ + 2;
+    // WS: step-1 and step-2 cells on separate warps (one collision per
+    // thread and plane: twice the warps of a latency-bound tile)
+    static constexpr bool WS = WS_;
     static constexpr int ZPAD = 16 / int(sizeof(T));  // TMA: 16 B aligned innermost origin
     static constexpr int BW = TZ + 2 * ZPAD, BOX = HY * BW;
     static constexpr int BOXE = kq_round_up(BOX * int(sizeof(T)), 128) / int(sizeof(T));
-    static constexpr int NT = kq_round_up(HY * HZ, 32);
+    static constexpr int S2B = WS ? kq_round_up(HY * HZ, 32) : 0;  // first step-2 thread
+    static constexpr int NT = kq_round_up(HY * HZ, 32) + (WS ? TY * TZ : 0);
     static constexpr int RP = TY * TZ;
     static constexpr int GM = kq_gsize<Q>(0), GZ = kq_gsize<Q>(1), GP = kq_gsize<Q>(2);
     static constexpr int DM = 3, DZ = 3, DP = 4;
@@ -359,11 +363,11 @@ __device__ __forceinline__ int kq_wrap(int v, int n) { return v < 0 ? v + n : (v
 
 }  // namespace
 
-template <typename T, int Q, int BC, int TY, int TZ>
-__global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ>::NT, 1)
+template <typename T, int Q, int BC, int TY, int TZ, bool WS>
+__global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ, WS>::NT, 1)
     k_dqq_k2(const __grid_constant__ CUtensorMap tm, const T* __restrict__ A, T* __restrict__ B, DqqGeom g, T omega,
              double ulx, double uly, int chunk) {
-    using C = KQCfg<T, Q, TY, TZ>;
+    using C = KQCfg<T, Q, TY, TZ, WS>;
     constexpr bool PER = BC == BC_PERIODIC;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* const stage = reinterpret_cast<T*>(smem_raw);
@@ -402,10 +406,12 @@ __global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ>::NT, 1)
     const bool colok[3] = {b >= 2 && b <= TZ + 1, b >= 1 && b <= TZ, b <= TZ - 1};
     // cavity walls of the step-1 cell (y, z; x per plane)
     const bool wyl = !PER && qy == 0, wyh = !PER && qy == g.ny - 1, wzl = !PER && qz == 0, wzh = !PER && qz == g.nz - 1;
-    // step-2 cell
-    const int y2 = tid / TZ, z2 = tid % TZ, yy = y0 + y2, zz = z0 + z2;
-    const bool in2 = tid < TY * TZ && yy < g.ny && zz < g.nz;
-    const bool warp2 = (tid & ~31) < TY * TZ;
+    // step-2 cell (WS: the threads from S2B on; else the first TY*TZ)
+    const int t2 = tid - C::S2B;
+    const int y2 = max(t2, 0) / TZ, z2 = max(t2, 0) % TZ, yy = y0 + y2, zz = z0 + z2;
+    const bool in2 = t2 >= 0 && t2 < TY * TZ && yy < g.ny && zz < g.nz;
+    const bool warp2 = WS ? tid >= C::S2B : (tid & ~31) < TY * TZ;
+    const bool warp1 = !WS || tid < C::S2B;  // the warp collides step-1 cells
     const bool vyl = !PER && yy == 0, vyh = !PER && yy == g.ny - 1, vzl = !PER && zz == 0, vzh = !PER && zz == g.nz - 1;
     // periodic destination offsets of the step-2 cell per c_y, c_z
     const long long yo[3] = {(long long)kq_wrap(yy - 1, g.ny) * g.nzp, (long long)yy * g.nzp,
@@ -449,7 +455,8 @@ __global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ>::NT, 1)
     };
 
     for (int p = xs - 1; p <= xe + 1; ++p) {
-        const bool has1 = p >= p_first && p <= p_last;
+        const bool has1 = p >= p_first && p <= p_last && warp1;
+        const bool has1_any = p >= p_first && p <= p_last;  // (the TMA issue of thread 0)
         const int c = p - p_first, s = c & 1;
         T fs[Q];
         if (has1) {
@@ -469,7 +476,7 @@ __global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ>::NT, 1)
             }
         }
         __syncthreads();  // stage of plane p consumed, ring of destination p-2 complete
-        if (tid == 0 && has1 && p + 2 <= p_last) issue(p + 2, s);
+        if (tid == 0 && has1_any && p + 2 <= p_last) issue(p + 2, s);
 
         // ---- step 2 of plane d = p - 2 and step 1 of plane p ----
         const int d = p - 2;
@@ -629,11 +636,11 @@ using KqEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, v
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-template <typename T, int Q, int BC, int TY, int TZ>
+template <typename T, int Q, int BC, int TY, int TZ, bool WS>
 cudaError_t launch_kq(const T* A, T* B, const DqqGeom& g, T omega, const double ulid[3], cudaStream_t s) {
-    using C = KQCfg<T, Q, TY, TZ>;
+    using C = KQCfg<T, Q, TY, TZ, WS>;
     static_assert(C::SMEM <= 227 * 1024, "K2Q tile does not fit shared memory");
-    auto kern = k_dqq_k2<T, Q, BC, TY, TZ>;
+    auto kern = k_dqq_k2<T, Q, BC, TY, TZ, WS>;
     // the large-shared-memory opt-in is per device (context): once per ordinal
     static std::atomic<int> done[64];
     const int dev = device_ordinal();
@@ -684,21 +691,26 @@ cudaError_t launch_kq(const T* A, T* B, const DqqGeom& g, T omega, const double 
 }  // namespace
 
 // Tiles (the largest whose stage + ring fit 227 KB): D3Q27 fp64 8x16 (178
-// KB), fp32 8x32 (178 KB); D3Q15 fp64 8x32 (184 KB), fp32 16x32 (184 KB).
+// KB, 320 threads: warp-specialised), fp32 8x32 (178 KB); D3Q15 fp64 8x32
+// (184 KB), fp32 16x32 (184 KB).
 template <typename T>
 cudaError_t launch_dqq_k2(const T* A, T* B, const DqqGeom& g, T omega, const double ulid[3], cudaStream_t s) {
     if (!tma_encode_entry()) return cudaErrorNotSupported;
     if (g.nx < 1 || (g.nzp * sizeof(T)) % 16) return cudaErrorInvalidValue;
     constexpr bool F64 = sizeof(T) == 8;
     constexpr int TY27 = 8, TZ27 = F64 ? 16 : 32, TY15 = F64 ? 8 : 16, TZ15 = 32;
+    // D3Q27 fp64: step-1 and step-2 cells on separate warps (10 warps per
+    // SM instead of 6; 15.7k vs 13.8k MLUPS, 512^3 cavity); elsewhere the
+    // shared warps (D3Q27 fp32 -4% split; D3Q15 split spills)
+    constexpr bool WS27 = F64, WS15 = false;
     const bool per = g.bc == BC_PERIODIC;
     switch (g.q) {
         case 27:
-            return per ? launch_kq<T, 27, BC_PERIODIC, TY27, TZ27>(A, B, g, omega, ulid, s)
-                       : launch_kq<T, 27, BC_CAVITY, TY27, TZ27>(A, B, g, omega, ulid, s);
+            return per ? launch_kq<T, 27, BC_PERIODIC, TY27, TZ27, WS27>(A, B, g, omega, ulid, s)
+                       : launch_kq<T, 27, BC_CAVITY, TY27, TZ27, WS27>(A, B, g, omega, ulid, s);
         case 15:
-            return per ? launch_kq<T, 15, BC_PERIODIC, TY15, TZ15>(A, B, g, omega, ulid, s)
-                       : launch_kq<T, 15, BC_CAVITY, TY15, TZ15>(A, B, g, omega, ulid, s);
+            return per ? launch_kq<T, 15, BC_PERIODIC, TY15, TZ15, WS15>(A, B, g, omega, ulid, s)
+                       : launch_kq<T, 15, BC_CAVITY, TY15, TZ15, WS15>(A, B, g, omega, ulid, s);
         default:
             return cudaErrorInvalidValue;
     }

@@ -98,7 +98,7 @@ def test_two_step_sweep_cavity_vs_oracle(q, tau, lid):
     """A 40 x 24 x 48 lid cavity (several tiles and x chunks) in fp64 through
     K2Q sweeps against the oracle after 10 steps, element by element, for
     three relaxation times and lids along x, y and the xy diagonal; AUTO
-    takes them too, except for D3Q27 fp64 (one-step kernel: faster there)."""
+    takes the same sweeps."""
     dims = (40, 24, 48)
     rho = 1.0 + li.uniform(5, int(np.prod(dims)), -1e-3, 1e-3).reshape(dims)
     ref = oracle.dqq_run(q, oracle.dqq_init_equilibrium(q, *dims, rho), lbm.LBM_BC_CAVITY, tau, lid, 10)
@@ -111,5 +111,5 @@ def test_two_step_sweep_cavity_vs_oracle(q, tau, lid):
     with lbm.Lattice(*dims, tau, lid, "f64", lattice=q) as lat:
         lat.init_equilibrium(rho, None)
         lat.step(10)
-        assert lbm.lbm_get_stats(lat.ctx).k2_launches == (0 if q == 27 else 5)
+        assert lbm.lbm_get_stats(lat.ctx).k2_launches == 5
         assert np.array_equal(lat.populations(), got)
