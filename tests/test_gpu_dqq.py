@@ -113,3 +113,21 @@ def test_two_step_sweep_cavity_vs_oracle(q, tau, lid):
         lat.step(10)
         assert lbm.lbm_get_stats(lat.ctx).k2_launches == 5
         assert np.array_equal(lat.populations(), got)
+
+
+def test_two_step_sweep_full_size_boxes_bitwise():
+    """D3Q27 fp64 on config 5's 1024 x 512 x 512 cavity (116 GB for two
+    copies: 64-bit slot offsets, 4D TMA coordinates, the x-chunk planner at
+    full size): 4 steps through K2Q equal 4 one-step launches bit for bit on
+    boxes at the corners, the lid, x-chunk seams and the interior."""
+    nx, ny, nz = 1024, 512, 512
+    rho = 1.0 + li.uniform(4, nx * ny * nz, -1e-3, 1e-3).reshape(nx, ny, nz)
+    boxes = [(0, 0, 0), (1021, 509, 508), (31, 255, 508), (511, 7, 250), (992, 500, 0)]
+    got = {}
+    for kern in (lbm.LBM_KERNEL_K2, lbm.LBM_KERNEL_K1):
+        with lbm.Lattice(nx, ny, nz, 0.6, LID, "f64", lattice=27, kernel=kern) as lat:
+            lat.init_equilibrium(rho, None)
+            lat.step(4)
+            got[kern] = [lat.populations_box(x, y, z, 3, 3, 4) for (x, y, z) in boxes]
+    for a, b in zip(got[lbm.LBM_KERNEL_K2], got[lbm.LBM_KERNEL_K1]):
+        assert np.array_equal(a, b)
