@@ -161,10 +161,12 @@ __device__ __forceinline__ void dqq_collide(T (&f)[Q], T omega) {
             // fp32 D3Q27: pairs j, j+1 of one weight class on packed FFMA2 /
             // FMUL2 / FADD2 (K2Q +4.5%, one-step +0.7%; D3Q15 K2Q -0.9%, so
             // D3Q15 stays scalar).  The packed form does not reproduce the
-            // scalar form's bits (measured: D3Q15 one-step packed vs K2Q
-            // scalar differ by a few ulp), so both kernels of a lattice use
-            // the same form and stay bitwise equal; both are within the
-            // oracle tolerance.
+            // scalar form's bits: ptxas (12.9, sm_100a) contracts the
+            // mul.rn.f32x2 / add.rn.f32x2 pairs into FFMA2 despite .rn (SASS:
+            // 9 mul + 6 add + 9 fma f32x2 in PTX become 6 FMUL2 + 15 FFMA2;
+            // each packed op alone is exact, tools/f32x2_probe.cu), so both
+            // kernels of a lattice use the same form and stay bitwise equal;
+            // both are within the oracle tolerance.
             constexpr int i2 = i + 1;
             const float owr = omega * (float(dqq_w<Q>(i)) * r);
             const float2 cu = make_float2(cdot(std::integral_constant<int, i>{}), cdot(std::integral_constant<int, i2>{}));
