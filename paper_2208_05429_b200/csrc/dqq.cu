@@ -721,9 +721,9 @@ cudaError_t launch_kq(const T* A, T* B, const DqqGeom& g, T omega, const double 
     const long long slots = device_sm_count();
     int best = 1;
     double best_cost = 1e300;
-    for (int nch = 1; nch <= g.nx; ++nch) {
+    for (int nch = 1; nch <= g.nx && nch <= 65535; ++nch) {  // (grid.y limit)
         const int ch = (g.nx + nch - 1) / nch;
-        if (ch > 32 && nch < g.nx) continue;
+        if (ch > 32 && nch < g.nx && nch < 65535) continue;
         const double waves = double((ntiles * ((g.nx + ch - 1) / ch) + slots - 1) / slots);
         const double cost = waves * (double(g.nx) / nch + 4.5);
         if (cost < best_cost - 1e-9) {

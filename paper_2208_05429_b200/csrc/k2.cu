@@ -752,9 +752,9 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     int best = 1;
     double best_cost = 1e300;
     const int ranges = nxs2 > 0 ? 2 : 1;
-    for (int nch = 1; nch <= nxs; ++nch) {
+    for (int nch = 1; nch <= nxs && nch * ranges <= 65535; ++nch) {  // (grid.y limit)
         const int chunk = (nxs + nch - 1) / nch;
-        if (chunk > kMaxChunk && nch < nxs) continue;
+        if (chunk > kMaxChunk && nch < nxs && (nch + 1) * ranges <= 65535) continue;
         const long long items = ntiles * ((nxs + chunk - 1) / chunk) * ranges;
         const double waves = double((items + slots - 1) / slots);
         // per CTA: its planes (the average chunk), ~2.5 recomputed step-1
