@@ -671,11 +671,21 @@ int num_sms() {
 }
 
 // x chunks of at most k2_max_chunk planes (launch_k2_impl): fp64 72 on
-// large cross-sections (`wide`), else 32 -- the single-copy ring always 32,
-// which sets its gap (k2_sc_gap); fp32 48
+// large cross-sections (`wide`), else 32 -- the single-copy ring its own
+// cap (k2_sc_max_chunk), which sets its gap (k2_sc_gap); fp32 48
 template <typename T>
 constexpr int k2_max_chunk(bool wide = false) {
     return sizeof(T) == 8 ? (wide ? 72 : 32) : 48;
+}
+#ifndef K2_SC_CHUNK
+#define K2_SC_CHUNK 72
+#endif
+// single-copy ring (K2_SC): its chunk cap, which sets the ring gap.  fp64
+// 72 planes (gap 148; bench K2 frac 0.764 -> 0.790 at 32 -> 72, 0.784 at
+// 56, interleaved A/B; +3.2 GB of ring for config 5), fp32 48
+template <typename T>
+constexpr int k2_sc_max_chunk() {
+    return (sizeof(T) == 8 && K2_SC_CHUNK > 0) ? K2_SC_CHUNK : k2_max_chunk<T>(false);
 }
 
 template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING, bool YB = false>
@@ -748,7 +758,7 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     // 2, with the z-strip tile order (less drift cost): the bench's K2 frac
     // 0.784 at 56, 0.785 at 64, 0.789 at 72-88, 0.787 at 96 -> 72.
     const bool wide = !RING && ntiles >= 4 * slots;
-    const int kMaxChunk = wide ? k2_max_chunk<T>(true) : k2_max_chunk<T>(false);
+    const int kMaxChunk = RING ? k2_sc_max_chunk<T>() : wide ? k2_max_chunk<T>(true) : k2_max_chunk<T>(false);
     int best = 1;
     double best_cost = 1e300;
     const int ranges = nxs2 > 0 ? 2 : 1;
@@ -822,7 +832,7 @@ bool k2_supported(const SlabGeom& g) {
 // what chunk j reads); chunks <= j-2 have finished (the ticket wait).
 template <typename T>
 int k2_sc_gap() {
-    return 2 * k2_max_chunk<T>(false) + 4;
+    return 2 * k2_sc_max_chunk<T>() + 4;
 }
 
 

@@ -25,7 +25,7 @@ for q, dims in [(q, d) for q in lattices for d in [(37, 45, 70), (20, 19, 97), (
             rho = (1 + 1e-3 * rng.uniform(-1, 1, (nx, ny, nz))).astype(np.float64)
             u = (0.02 * rng.uniform(-1, 1, (nx, ny, nz, 3))).astype(np.float64)
             out = []
-            for kern in (1, 2):
+            for kern in [int(v) for v in os.environ.get("AB_KERNELS", "1,2").split(",")]:
                 with lbm.Lattice(nx, ny, nz, 0.6, (0.05, 0, 0), dt, bc=bc, kernel=kern, lattice=q) as lat:
                     lat.init_equilibrium(rho, u)
                     lat.step(6)
