@@ -127,11 +127,12 @@ typedef enum {
     /* Single-copy storage with the two-step merge -- the paper's pairing of
      * one lattice copy with two steps per pass (
      * SURVEY.md 8(f) row 1).  The K2 sweep runs in place: the lattice is a
-     * ring of nx + 4 + G planes (G = 148 fp64 / 100 fp32; 1.14x a single copy
-     * at nx = 1024, plus a staging buffer of max(3 planes, 64 MB, 1/16 of the
-     * lattice) for host transfers) and each sweep writes f*(t+1) of plane x
-     * G planes below the slot of f*(t-1) of plane x, chunks of <= 32 (48)
-     * planes taken in x order, so no plane is overwritten before its last
+     * ring of nx + 4 + G planes (G = 68 fp64, 148 on slabs of >= 1024
+     * planes, 100 fp32; 1.14x a single copy at nx = 1024, plus a staging
+     * buffer of max(3 planes, 64 MB, 1/16 of the lattice) for host
+     * transfers) and each sweep writes f*(t+1) of plane x G planes below the
+     * slot of f*(t-1) of plane x, chunks of <= (G - 4) / 2 planes
+     * taken in x order, so no plane is overwritten before its last
      * reader has finished; an odd step runs the in-place K1 the same way.
      * Bitwise identical to K2/K1.  X-slabs (LOCAL, NCCL): each slab its own
      * ring, halo parts exchanged through the ring mapping; init and

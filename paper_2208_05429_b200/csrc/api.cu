@@ -2087,7 +2087,7 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         lbm_halo_plan tp;
         fill_plan(nx, ny, nz, es_, o.bc, 0, nslab_total, nxl, 0, &tp);
         const size_t plane_x = size_t(tp.plane_x) * es_;
-        const size_t gap = size_t(dt == LBM_F64 ? k2_sc_gap<double>() : k2_sc_gap<float>());
+        const size_t gap = size_t(dt == LBM_F64 ? k2_sc_gap<double>(nxl) : k2_sc_gap<float>(nxl));
         const size_t two = size_t(sw) * 2 * (size_t(nxl) + 4) * plane_x;
         const size_t lattice = (size_t(nxl) + 4) * plane_x;
         const size_t stage =
@@ -2147,7 +2147,7 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
         s.g.pmod = nxl + 4;
         if (use_sc) {
             c->sc = true;
-            c->sc_gap = dt == LBM_F64 ? k2_sc_gap<double>() : k2_sc_gap<float>();
+            c->sc_gap = dt == LBM_F64 ? k2_sc_gap<double>(nxl) : k2_sc_gap<float>(nxl);
             s.g.pmod = nxl + 4 + c->sc_gap;
             const bool ok = dt == LBM_F64 ? k2_supported<double>(s.g) : k2_supported<float>(s.g);
             if (!ok && o.kernel == LBM_KERNEL_K2_SC)

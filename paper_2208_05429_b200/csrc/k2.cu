@@ -677,15 +677,14 @@ template <typename T>
 constexpr int k2_max_chunk(bool wide = false) {
     return sizeof(T) == 8 ? (wide ? 72 : 32) : 48;
 }
-#ifndef K2_SC_CHUNK
-#define K2_SC_CHUNK 72
-#endif
-// single-copy ring (K2_SC): its chunk cap, which sets the ring gap.  fp64
-// 72 planes (gap 148; bench K2 frac 0.764 -> 0.790 at 32 -> 72, 0.784 at
-// 56, interleaved A/B; +3.2 GB of ring for config 5), fp32 48
+// single-copy ring (K2_SC): its chunk cap, which sets the ring gap (the
+// ring's extra planes).  fp64 72 planes (gap 148) on slabs of >= 1024
+// planes, where the gap costs <= 14% of a lattice copy (bench K2_SC frac
+// 0.764 -> 0.790 at 32 -> 72 on config 5, 0.784 at 56: interleaved A/B),
+// else 32 (gap 68: a short slab keeps its ring close to one copy); fp32 48
 template <typename T>
-constexpr int k2_sc_max_chunk() {
-    return (sizeof(T) == 8 && K2_SC_CHUNK > 0) ? K2_SC_CHUNK : k2_max_chunk<T>(false);
+constexpr int k2_sc_max_chunk(int nxl) {
+    return (sizeof(T) == 8 && nxl >= 1024) ? 72 : k2_max_chunk<T>(false);
 }
 
 template <typename T, int BC, int TY, int TZ, bool EARLY, bool RING, bool YB = false>
@@ -758,7 +757,9 @@ cudaError_t launch_k2_impl(const T* A, T* B, const StepParams<T>& P, int xbeg, i
     // 2, with the z-strip tile order (less drift cost): the bench's K2 frac
     // 0.784 at 56, 0.785 at 64, 0.789 at 72-88, 0.787 at 96 -> 72.
     const bool wide = !RING && ntiles >= 4 * slots;
-    const int kMaxChunk = RING ? k2_sc_max_chunk<T>() : wide ? k2_max_chunk<T>(true) : k2_max_chunk<T>(false);
+    // (ring: the cap its gap was sized for, gap = pmod - nxl - 4 = 2 cap + 4)
+    const int kMaxChunk = RING ? std::max(1, (g.pmod - g.nxl - 8) / 2)
+                               : wide ? k2_max_chunk<T>(true) : k2_max_chunk<T>(false);
     int best = 1;
     double best_cost = 1e300;
     const int ranges = nxs2 > 0 ? 2 : 1;
@@ -831,8 +832,8 @@ bool k2_supported(const SlabGeom& g) {
 // j-1 and later no longer read iff gap >= 2L + 2 ([jL - 2, (j+1)L + 1] is
 // what chunk j reads); chunks <= j-2 have finished (the ticket wait).
 template <typename T>
-int k2_sc_gap() {
-    return 2 * k2_sc_max_chunk<T>() + 4;
+int k2_sc_gap(int nxl) {
+    return 2 * k2_sc_max_chunk<T>(nxl) + 4;
 }
 
 
@@ -893,7 +894,7 @@ template cudaError_t launch_k2<double>(const double*, double*, const StepParams<
                                        int, unsigned*, double*, double*, int, int);
 template cudaError_t launch_k2<float>(const float*, float*, const StepParams<float>&, int, int, cudaStream_t, int,
                                       unsigned*, float*, float*, int, int);
-template int k2_sc_gap<double>();
-template int k2_sc_gap<float>();
+template int k2_sc_gap<double>(int);
+template int k2_sc_gap<float>(int);
 
 }  // namespace lbm

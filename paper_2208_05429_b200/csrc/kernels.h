@@ -38,7 +38,7 @@ cudaError_t launch_k2(const T* A, T* B, const StepParams<T>& P, int xbeg, int nx
                       unsigned* sc_sync = nullptr, T* halo_left = nullptr, T* halo_right = nullptr, int xbeg2 = 0,
                       int nxs2 = 0);
 template <typename T>
-int k2_sc_gap();
+int k2_sc_gap(int nxl);  // the ring's extra planes for a slab of nxl planes
 template <typename T>
 bool k2_supported(const SlabGeom& g);
 
