@@ -192,3 +192,38 @@ def test_shear_wave_viscosity(q, tau):
     g1 = oracle.dqq_run(q, g0, oracle.BC_PERIODIC, tau, (0, 0, 0), t1 - t0)
     nu = -math.log(amp(g1) / amp(g0)) / ((2 * np.pi / L) ** 2 * (t1 - t0))
     assert abs(nu / ((tau - 0.5) / 3) - 1) <= 3e-3
+
+
+@pytest.mark.parametrize("q", [15, 27])
+def test_paired_collision_identities(q):
+    """R-16's reading (the GPU's paired-direction collision for these
+    lattices) rests on identities of the velocity set, checked here in exact
+    rational arithmetic on the oracle's own table: the table is closed under
+    c -> -c with opp(i) = i + (q-1)/2; within each weight class (|c|^2 = 1,
+    2, 3) the half set's sum of (c.u)^2 is k_c u.u with k = 1, 4, 4 for
+    every u; so sum_{i>0} feq_i = 2 sum_c w_c rho (n_c (1 - 1.5 u.u) +
+    4.5 k_c u.u) equals rho - feq_0 exactly (the closed-form closure)."""
+    c, w, _ = oracle.dqq_table(q)
+    c = np.asarray(c, dtype=int).reshape(q, 3)
+    w = [Fraction(x).limit_denominator(1000) for x in w]
+    h = (q - 1) // 2
+    for i in range(1, h + 1):
+        assert all(c[i + h] == -c[i]) and w[i + h] == w[i]
+    rng = np.random.default_rng(16)
+    for _ in range(5):
+        u = [Fraction(int(v), 997) for v in rng.integers(-60, 60, 3)]
+        rho = Fraction(int(rng.integers(900, 1100)), 1000)
+        usq = sum(x * x for x in u)
+        base = 1 - Fraction(3, 2) * usq
+        cu = [sum(int(c[i][a]) * u[a] for a in range(3)) for i in range(q)]
+        clos = Fraction(0)
+        for n2, k in ((1, 1), (2, 4), (3, 4)):
+            half = [i for i in range(1, h + 1) if int(c[i] @ c[i]) == n2]
+            if not half:
+                continue
+            assert sum(cu[i] ** 2 for i in half) == k * usq
+            assert len({w[i] for i in half}) == 1
+            clos += w[half[0]] * rho * (len(half) * base + Fraction(9, 2) * k * usq)
+        feq = [w[i] * rho * (1 + 3 * cu[i] + Fraction(9, 2) * cu[i] ** 2 - Fraction(3, 2) * usq) for i in range(q)]
+        assert 2 * clos == sum(feq[1:])
+        assert rho - 2 * clos == feq[0]
