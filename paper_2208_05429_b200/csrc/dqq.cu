@@ -27,6 +27,10 @@
 
 #include "kernels.h"
 
+#ifndef KQ_FAST
+#define KQ_FAST 1
+#endif
+
 namespace lbm {
 
 namespace {
@@ -463,6 +467,9 @@ __global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ, WS>::NT, 1)
     const bool warp2 = WS ? tid >= C::S2B : (tid & ~31) < TY * TZ;
     const bool warp1 = !WS || tid < C::S2B;  // the warp collides step-1 cells
     const bool vyl = !PER && yy == 0, vyh = !PER && yy == g.ny - 1, vzl = !PER && zz == 0, vzh = !PER && zz == g.nz - 1;
+    // no tile cell on a y / z wall (CTA-uniform): its planes away from the x
+    // walls push every link plainly -- no per-direction wall test or branch
+    const bool tile_inner = !PER && y0 >= 1 && y0 + TY <= g.ny - 1 && z0 >= 1 && z0 + TZ <= g.nz - 1;
     // periodic destination offsets of the step-2 cell per c_y, c_z
     const long long yo[3] = {(long long)kq_wrap(yy - 1, g.ny) * g.nzp, (long long)yy * g.nzp,
                              (long long)kq_wrap(yy + 1, g.ny) * g.nzp};
@@ -541,7 +548,14 @@ __global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ, WS>::NT, 1)
         }
         if (do2) dqq_collide<T, Q>(f2, omega);
         if (has1) dqq_collide<T, Q>(fs, omega);
-        if (do2 && in2) {
+        if (do2 && in2 && KQ_FAST && tile_inner && d > 0 && d < g.nx - 1) {
+            const long long own = (long long)d * plane + (long long)yy * g.nzp + zz;
+            static_for<0, Q>([&](auto kc) {
+                constexpr int i = decltype(kc)::value;
+                constexpr int cx = dqq_c<Q>(i, 0), cy = dqq_c<Q>(i, 1), cz = dqq_c<Q>(i, 2);
+                __stcs(B + (long long)i * g.pq + own + (long long)cx * plane + cy * g.nzp + cz, f2[i]);
+            });
+        } else if (do2 && in2) {
             const long long own = (long long)d * plane + (long long)yy * g.nzp + zz;
             const bool vxl = !PER && d == 0, vxh = !PER && d == g.nx - 1;
             const long long xo[3] = {(long long)kq_wrap(d - 1, g.nx) * plane, (long long)d * plane,
@@ -586,7 +600,7 @@ __global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ, WS>::NT, 1)
             });
             if constexpr (!PER) {
                 // links of a tile cell that leave the domain: bounce-back (+ lid) into its own slot
-                if (q_tile) {
+                if (q_tile && !(KQ_FAST && tile_inner && p > 0 && p < g.nx - 1)) {
                     const bool wxl = p == 0, wxh = p == g.nx - 1;
                     static_for<0, Q>([&](auto kc) {
                         constexpr int i = decltype(kc)::value;
