@@ -186,6 +186,8 @@ def main():
     ap.add_argument("--dims", default=None, help="override NX,NY,NZ (profiling runs only)")
     ap.add_argument("--weak", action="store_true",
                     help="weak scaling (BASELINE.json:11): 128 x 512 x 512 cells of config 5 per GPU")
+    ap.add_argument("--lattice", type=int, default=19, choices=[15, 19, 27],
+                    help="velocity set: D3Q19 (the paper's, default) or D3Q15 / D3Q27 (one GPU; DESIGN.md section 11)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -203,7 +205,10 @@ def main():
             ap.error("--weak is config 5's weak-scaling series (128x512x512 per GPU)")
         cfg = cfg.with_dims(128 * max(1, int(os.environ.get("WORLD_SIZE", "1"))), cfg.ny, cfg.nz)
     if args.impl == "reference":
+        if args.lattice != 19:
+            ap.error("--impl reference times the D3Q19 oracle (the paper's lattice)")
         return run_reference(args, cfg)
+    Q = args.lattice
 
     import torch
     import torch.distributed as dist
@@ -221,6 +226,8 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
     ry = args.ranks_y if world > 1 else 1
+    if Q != 19 and world > 1:
+        ap.error("--lattice 15 / 27 run on one slab (one GPU)")
     if world % ry or cfg.ny % ry:
         ap.error("--ranks-y must divide the world size and ny")
     nxl = cfg.nx // (world // ry)
@@ -242,7 +249,7 @@ def main():
                       comm=lbm.LBM_COMM_NCCL if world > 1 else lbm.LBM_COMM_NONE, rank=rank, world=world,
                       nccl_id=nccl_id, stream=stream.cuda_stream, device=local_rank,
                       halo=lbm.LBM_HALO_PEER if (args.halo == "peer" and world > 1) else lbm.LBM_HALO_AUTO,
-                      ranks_y=ry)
+                      ranks_y=ry, lattice=Q)
     ctx = lat.ctx
 
     # inputs: this rank's slab of the config's seeded fields, resident in HBM
@@ -312,7 +319,7 @@ def main():
     launches = s1.launches - s0.launches
 
     # dominant kernel: the sweep (K2 two-step, or K1) -- algorithmic bytes per launch
-    # = cells in the launch x 2 x 19 x sizeof(T) (each population read once and written once)
+    # = cells in the launch x 2 x Q x sizeof(T) (each population read once and written once)
     es = ESIZE[args.dtype]
     sweep_ms = s1.sweep_ms
     sweep_launches = s1.sweep_launches
@@ -321,8 +328,10 @@ def main():
     k1 = s1.k1_launches - s0.k1_launches
     dominant = (({"k2sc": "k2_single_copy", "k3": "k3_three_step"}.get(args.kernel, "k2_two_step")) if k2 >= k1
                 else ("aa_step" if args.kernel == "aa" else "k1_step"))
-    # per launch: cells_local x 2 x 19 x es bytes (both K1 and K2 stream the lattice once)
-    bytes_per_launch = cells_local * 2 * 19 * es
+    if Q != 19:
+        dominant = f"d3q{Q}_" + ("k2q_two_step" if k2 >= k1 else "one_step")
+    # per launch: cells_local x 2 x Q x es bytes (both K1 and K2 stream the lattice once)
+    bytes_per_launch = cells_local * 2 * Q * es
     avg_launch_ms = sweep_ms / max(1, sweep_launches)
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
@@ -345,7 +354,10 @@ def main():
                "d2h_bytes_per_step": int(out_rho_h.numel() * 8 + out_u_h.numel() * 8) * world}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the contract: rank 0 at N=1 only
+    if Q != 19 and not args.no_cpu_baseline:
+        cpu = {"value": None, "unit": "MLUPS", "cores": None, "kind": "oracle",
+               "sample": "not timed: the CPU baseline is the D3Q19 oracle's"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:  # the contract: rank 0 at N=1 only
         try:
             v, threads, sample, _ = oracle_sample(cfg, 12.0)
             model, ncpu = cpu_info()
@@ -360,7 +372,7 @@ def main():
     for tf in ("r02c_traffic.json", "r02b_traffic.json", "r02_traffic.json", "r01_traffic.json"):
         try:
             tj = json.load(open(os.path.join(ROOT, "profiles", tf)))
-            t = tj.get(cfg.name, {}).get(dominant, {}).get(args.dtype) if world == 1 else None
+            t = tj.get(cfg.name, {}).get(dominant, {}).get(args.dtype) if (world == 1 and Q == 19) else None
             if t:
                 traffic = {"bytes_per_launch": t["read"] + t["write"], "read": t["read"], "write": t["write"],
                            "x_algorithmic": round((t["read"] + t["write"]) / bytes_per_launch, 3),
@@ -370,7 +382,7 @@ def main():
             continue
 
     if rank == 0:
-        mlups_bytes = 2 * 19 * es  # BASELINE.json:5 roofline: MLUPS x single-step bytes / peak
+        mlups_bytes = 2 * Q * es  # BASELINE.json:5 roofline: MLUPS x single-step bytes / peak
         line = {
             "metric": "MLUPS", "value": round(value, 3), "unit": "MLUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
@@ -382,7 +394,8 @@ def main():
                        "inputs": ("rho (u is identically 0: passed as NULL)" if u_zero else "rho, u"),
                        "kernel": args.kernel, "parallelism": f"x-slab{world}" if ry == 1 else f"xy-block{world // ry}x{ry}",
                        "halo": args.halo if world > 1 else "none",
-                       "l2": f"inputs larger than L2: {cells_local * 19 * es / 1e9:.1f} GB per lattice copy per GPU"},
+                       "l2": f"inputs larger than L2: {cells_local * Q * es / 1e9:.1f} GB per lattice copy per GPU",
+                       "lattice": f"D3Q{Q}"},
             "mlups_per_gpu": round(value / world, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
