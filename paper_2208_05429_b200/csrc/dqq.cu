@@ -395,6 +395,7 @@ struct KQCfg {
     static constexpr int RING = (DM * GM + DZ * GZ + DP * GP) * RP;
     static constexpr size_t SMEM = size_t(2 * Q * BOXE + RING) * sizeof(T) + 2 * sizeof(uint64_t);
     static constexpr uint32_t TX = uint32_t(Q * BOX * sizeof(T));
+    static constexpr int MINB = SMEM + 1024 <= 114 * 1024 ? 2 : 1;  // CTAs per SM that shared memory allows
 };
 
 __device__ __forceinline__ uint32_t kq_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -418,7 +419,7 @@ __device__ __forceinline__ int kq_wrap(int v, int n) { return v < 0 ? v + n : (v
 }  // namespace
 
 template <typename T, int Q, int BC, int TY, int TZ, bool WS>
-__global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ, WS>::NT, 1)
+__global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ, WS>::NT, KQCfg<T, Q, TY, TZ, WS>::MINB)
     k_dqq_k2(const __grid_constant__ CUtensorMap tm, const T* __restrict__ A, T* __restrict__ B, DqqGeom g, T omega,
              double ulx, double uly, int chunk) {
     using C = KQCfg<T, Q, TY, TZ, WS>;
@@ -706,12 +707,16 @@ cudaError_t launch_kq(const T* A, T* B, const DqqGeom& g, T omega, const double 
     static_assert(C::SMEM <= 227 * 1024, "K2Q tile does not fit shared memory");
     auto kern = k_dqq_k2<T, Q, BC, TY, TZ, WS>;
     // the large-shared-memory opt-in is per device (context): once per ordinal
-    static std::atomic<int> done[64];
+    static std::atomic<int> occ_cache[64];  // CTAs per SM, once the opt-in is set (per device)
     const int dev = device_ordinal();
-    if (!done[dev].load(std::memory_order_acquire)) {
+    int occ = occ_cache[dev].load(std::memory_order_acquire);
+    if (occ < 1) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
         if (e != cudaSuccess) return e;
-        done[dev].store(1, std::memory_order_release);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, C::SMEM);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) return cudaErrorInvalidConfiguration;
+        occ_cache[dev].store(occ, std::memory_order_release);
     }
     auto enc = reinterpret_cast<KqEncodeFn>(tma_encode_entry());
     if (!enc) return cudaErrorNotSupported;
@@ -732,7 +737,7 @@ cudaError_t launch_kq(const T* A, T* B, const DqqGeom& g, T omega, const double 
     // filling whole waves of one CTA per SM; each chunk re-computes ~2.5
     // step-1 planes and ~2 planes of pipeline fill
     const long long ntiles = (long long)((g.ny + TY - 1) / TY) * ((g.nz + TZ - 1) / TZ);
-    const long long slots = device_sm_count();
+    const long long slots = (long long)device_sm_count() * occ;
     int best = 1;
     double best_cost = 1e300;
     for (int nch = 1; nch <= g.nx && nch <= 65535; ++nch) {  // (grid.y limit)
@@ -755,8 +760,9 @@ cudaError_t launch_kq(const T* A, T* B, const DqqGeom& g, T omega, const double 
 }  // namespace
 
 // Tiles (the largest whose stage + ring fit 227 KB): D3Q27 fp64 8x16 (178
-// KB, 320 threads: warp-specialised), fp32 8x32 (178 KB); D3Q15 fp64 8x32
-// (184 KB), fp32 16x32 (184 KB).
+// KB, 320 threads: warp-specialised), fp32 8x32 (178 KB; an 8x16 tile with
+// two CTAs per SM measured 8% slower); D3Q15 fp64 8x32 (184 KB), fp32
+// 16x32 (184 KB).
 template <typename T>
 cudaError_t launch_dqq_k2(const T* A, T* B, const DqqGeom& g, T omega, const double ulid[3], cudaStream_t s) {
     if (!tma_encode_entry()) return cudaErrorNotSupported;
