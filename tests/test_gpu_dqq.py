@@ -131,3 +131,23 @@ def test_two_step_sweep_full_size_boxes_bitwise():
             got[kern] = [lat.populations_box(x, y, z, 3, 3, 4) for (x, y, z) in boxes]
     for a, b in zip(got[lbm.LBM_KERNEL_K2], got[lbm.LBM_KERNEL_K1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("q", [15, 27])
+@pytest.mark.parametrize("dims,bc", [((1, 9, 40), lbm.LBM_BC_CAVITY), ((5, 1, 33), lbm.LBM_BC_CAVITY),
+                                     ((4, 7, 1), lbm.LBM_BC_CAVITY), ((2, 1, 40), lbm.LBM_BC_PERIODIC),
+                                     ((3, 9, 1), lbm.LBM_BC_PERIODIC), ((33, 2, 2), lbm.LBM_BC_PERIODIC)])
+def test_two_step_sweep_degenerate_extents(q, dims, bc):
+    """K2Q on one-plane, one-row and one-column lattices (every link of a
+    one-cell extent bounces, or wraps onto the cell itself): bitwise equal to
+    the one-step kernel and within 1e-12 of the oracle after 4 steps."""
+    f0 = li.uniform(120 + q, q * int(np.prod(dims)), 0.01, 0.06).reshape(q, *dims)
+    outs = []
+    for kern in (lbm.LBM_KERNEL_K1, lbm.LBM_KERNEL_K2):
+        with lbm.Lattice(*dims, 0.6, LID, "f64", bc=bc, lattice=q, kernel=kern) as lat:
+            lat.set_populations(f0)
+            lat.step(4)
+            outs.append(lat.populations())
+    assert np.array_equal(outs[0], outs[1])
+    ref = oracle.dqq_run(q, f0, bc, 0.6, LID, 4)
+    assert relerr_floor(outs[1], ref) <= TOL["f64"]
