@@ -25,3 +25,12 @@ def test_reference_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["value"] == d["value"] and cb["cores"] >= 1 and cb["sample"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_reference_arm_rejects_other_lattices():
+    """The reference arm times the D3Q19 oracle only; `--lattice 15|27` with
+    `--impl reference` is a usage error (exit 2), not a silent D3Q19 run."""
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--lattice", "27",
+                          "--steps", "1", "--warmup", "1"], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 2 and "D3Q19 oracle" in out.stderr
