@@ -34,3 +34,19 @@ def test_reference_arm_rejects_other_lattices():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--lattice", "27",
                           "--steps", "1", "--warmup", "1"], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 2 and "D3Q19 oracle" in out.stderr
+
+
+def test_reference_arm_under_torchrun_world2():
+    """Launched as the driver launches N > 1 (torchrun, two ranks): rank 0
+    alone times the oracle and prints the one JSON line; rank 1 exits 0
+    without work."""
+    env = dict(os.environ, LBM_REF_BUDGET_S="0.5", PYTHONPATH=ROOT)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "bench.py"),
+                          "--impl", "reference", "--gpus", "2", "--config", "2", "--steps", "1", "--warmup", "1"],
+                         env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
