@@ -768,7 +768,10 @@ cudaError_t launch_dqq_k2(const T* A, T* B, const DqqGeom& g, T omega, const dou
     if (!tma_encode_entry()) return cudaErrorNotSupported;
     if (g.nx < 1 || (g.nzp * sizeof(T)) % 16) return cudaErrorInvalidValue;
     constexpr bool F64 = sizeof(T) == 8;
-    constexpr int TY27 = 8, TZ27 = F64 ? 16 : 32, TY15 = F64 ? 8 : 16, TZ15 = 32;
+#ifndef LBM_KQ27_F64_TZ
+#define LBM_KQ27_F64_TZ 16  // (A/B builds override: tools/build_variant.sh -DLBM_KQ27_F64_TZ=8)
+#endif
+    constexpr int TY27 = 8, TZ27 = F64 ? LBM_KQ27_F64_TZ : 32, TY15 = F64 ? 8 : 16, TZ15 = 32;
     // D3Q27 fp64: step-1 and step-2 cells on separate warps (10 warps per
     // SM instead of 6; 15.7k vs 13.8k MLUPS, 512^3 cavity); elsewhere the
     // shared warps (D3Q27 fp32 -4% split; D3Q15 split spills)
