@@ -288,3 +288,20 @@ def test_plan_halo_xy(bc):
     for bad in ((4, 3), (6, 4)):  # world % ranks_y, ny % ranks_y (ny = 32 ok for 2) -> nx / ny checks
         with pytest.raises(lbm.LbmError):
             lbm.lbm_plan_halo_xy(nx, 30, nz, "f64", bc, 0, bad[0], bad[1])
+
+
+def test_binding_fails_loudly_without_library(tmp_path):
+    """No CPU fallback: a package copy without liblbm_b200.so raises
+    ImportError at import (the product path never routes elsewhere)."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = tmp_path / "paper_2208_05429_b200"
+    pkg.mkdir()
+    src = os.path.join(ROOT, "paper_2208_05429_b200")
+    for f in ("__init__.py", "build.py"):
+        shutil.copy(os.path.join(src, f), pkg / f)
+    out = subprocess.run([sys.executable, "-c", "import paper_2208_05429_b200"], cwd=tmp_path,
+                         env=dict(os.environ, PYTHONPATH=str(tmp_path)), capture_output=True, text=True, timeout=120)
+    assert out.returncode != 0
+    assert "ImportError" in out.stderr and "liblbm_b200.so is missing" in out.stderr
