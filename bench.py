@@ -187,7 +187,7 @@ def main():
     ap.add_argument("--weak", action="store_true",
                     help="weak scaling (BASELINE.json:11): 128 x 512 x 512 cells of config 5 per GPU")
     ap.add_argument("--lattice", type=int, default=19, choices=[15, 19, 27],
-                    help="velocity set: D3Q19 (the paper's, default) or D3Q15 / D3Q27 (one GPU; DESIGN.md section 11)")
+                    help="velocity set: D3Q19 (the paper's, default) or D3Q15 / D3Q27 (N > 1: x slabs, one-step kernel; DESIGN.md section 11)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -226,8 +226,8 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
     ry = args.ranks_y if world > 1 else 1
-    if Q != 19 and world > 1:
-        ap.error("--lattice 15 / 27 run on one slab (one GPU)")
+    if Q != 19 and world > 1 and (args.ranks_y > 1 or args.halo == "peer" or args.kernel not in ("auto", "k1")):
+        ap.error("--lattice 15 / 27 across GPUs: x slabs over NCCL send/recv, one-step kernel (auto or k1)")
     if world % ry or cfg.ny % ry:
         ap.error("--ranks-y must divide the world size and ny")
     nxl = cfg.nx // (world // ry)

@@ -199,7 +199,14 @@ typedef enum { LBM_HALO_AUTO = 0, LBM_HALO_EXCHANGE = 1, LBM_HALO_PEER = 2 } lbm
  * (the paper's merge for these lattices; ECUDA under K2
  * if the driver cannot encode TMA descriptors, AUTO then falls back), an
  * odd remainder and kernel K1 one fused collide + stream step per pass;
- * the results are bitwise the same.  Host population arrays
+ * the results are bitwise the same.  Across NCCL ranks (comm NCCL, x slabs
+ * only: local_slabs 1, ranks_y 1, halo AUTO or EXCHANGE; kernel AUTO or
+ * K1, K2 is EINVAL) every step is the one-step kernel: links leaving the
+ * slab through a face shared with a neighbour rank land in a ghost plane
+ * and are sent to that rank after the step (one ncclSend/ncclRecv per
+ * direction with c_x = +-1; a one-rank periodic box sends its wrap to
+ * itself); host arrays then cover the rank's slab, as for D3Q19, and input
+ * validation is agreed across ranks.  Host population arrays
  * are f[q][nx][ny][nz] in the order lbm_lattice_table gives: i = 0 rest,
  * 1 .. (q-1)/2 the velocities whose first nonzero component is -1 (axes,
  * face diagonals, corners), then their opposites in the same order -- for

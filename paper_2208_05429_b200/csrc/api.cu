@@ -165,7 +165,10 @@ struct lbm_ctx {
     // ping-pong buffers, one fused collide + push step per launch
     int q = 19;
     DqqGeom dg{};
-    void* dbuf[2] = {nullptr, nullptr};
+    void* dbuf[2] = {nullptr, nullptr};   // cell (0, 0, 0) of slot 0 (NCCL slabs: past the ghost plane)
+    void* dbase[2] = {nullptr, nullptr};  // the allocations
+    long long dorg = 0;                   // elements from dbase to dbuf (one ghost plane, or 0)
+    int dleft = -1, dright = -1;          // NCCL X-slab neighbour ranks of a D3Q15/27 slab (-1: wall / none)
     int dcur = 0;
     size_t esize = 8;
     int* d_flag = nullptr;
@@ -1627,20 +1630,23 @@ lbm_status dqq_init(lbm_ctx* c, const double* rho, const double* u, bool host) {
     if (host) {
         double* stage = static_cast<double*>(c->dbuf[c->dcur ^ 1]);
         dr = du = nullptr;
-        int flag = 0;
+        int flag = 0, bad = 0;
+        const char* why = nullptr;
         lbm_status st;
         if (rho) {
             CK(cudaMemcpyAsync(stage, rho, cells * sizeof(double), cudaMemcpyHostToDevice, c->stream));
             dr = stage;
             if ((st = validate_device(c, dr, cells, true, &flag)) != LBM_OK) return st;
-            if (flag) return fail(c, LBM_EINVAL, "rho must be finite and > 0");
+            if (flag) bad = 1, why = "rho must be finite and > 0";
         }
-        if (u) {
+        if (u && !bad) {
             CK(cudaMemcpyAsync(stage + cells, u, 3 * cells * sizeof(double), cudaMemcpyHostToDevice, c->stream));
             du = stage + cells;
             if ((st = validate_device(c, du, 3 * cells, false, &flag)) != LBM_OK) return st;
-            if (flag) return fail(c, LBM_EINVAL, "u must be finite");
+            if (flag) bad = 1, why = "u must be finite";
         }
+        // NCCL slabs: every rank learns the verdict before any exchange
+        if ((st = agree_valid(c, bad, why)) != LBM_OK) return st;
     }
     CK(launch_dqq_init<T>(dr, du, A, g, c->stream));
     c->launches++;
@@ -1654,9 +1660,10 @@ lbm_status dqq_set(lbm_ctx* c, const double* f) {
     c->initialized = false;
     const DqqGeom& g = c->dg;
     const long long plane = (long long)g.ny * g.nz, cells = (long long)g.nx * plane;
-    const size_t stage_bytes = size_t(g.q) * size_t(g.pq) * c->esize;
+    const size_t stage_bytes = (size_t(g.q) * size_t(g.pq) - size_t(c->dorg)) * c->esize;
     const int cap = int(std::max<long long>(1, (long long)(stage_bytes / (size_t(g.q) * plane * sizeof(double)))));
     double* stage = static_cast<double*>(c->dbuf[c->dcur ^ 1]);
+    int bad = 0;
     for (int xb = 0; xb < g.nx; xb += cap) {
         const int nxc = std::min(cap, g.nx - xb);
         const long long cc = (long long)nxc * plane;
@@ -1665,13 +1672,46 @@ lbm_status dqq_set(lbm_ctx* c, const double* f) {
         int flag = 0;
         lbm_status st = validate_device(c, stage, g.q * cc, false, &flag);
         if (st != LBM_OK) return st;
-        if (flag) return fail(c, LBM_EINVAL, "populations must be finite (state is now undefined)");
-        CK(launch_dqq_import<T>(stage, static_cast<T*>(c->dbuf[c->dcur]), g, xb, nxc, c->stream));
-        c->launches++;
+        bad |= flag;
+        if (!bad) {
+            CK(launch_dqq_import<T>(stage, static_cast<T*>(c->dbuf[c->dcur]), g, xb, nxc, c->stream));
+            c->launches++;
+        }
     }
+    // (NCCL slabs: every rank learns the verdict)
+    if (lbm_status st = agree_valid(c, bad, bad ? "populations must be finite" : nullptr); st != LBM_OK) return st;
     c->initialized = true;
     c->t = 0;
     return LBM_OK;
+}
+
+// X-slab halo of a D3Q15/27 NCCL slab after a push step (B = f(t+1)): the
+// populations pushed into ghost plane x = nx (c_x = +1) belong to plane 0
+// of the right neighbour, those in ghost plane x = -1 (c_x = -1) to plane
+// nx - 1 of the left one -- per direction one contiguous (y, z) plane,
+// which no rank writes otherwise (its source lies across the face)
+template <typename T>
+lbm_status dqq_exchange(lbm_ctx* c, T* B) {
+    const DqqGeom& g = c->dg;
+    const long long plane = (long long)g.ny * g.nzp;
+    const ncclDataType_t ty = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+    int cv[27 * 3];
+    double wv[27];
+    dqq_table(g.q, cv, wv);
+    CKN(g_nccl.GroupStart());
+    for (int i = 0; i < g.q; ++i) {
+        T* const slot = B + (long long)i * g.pq;
+        if (cv[3 * i] == 1) {  // [send right, recv left]: pairs match when left == right (two ranks, or itself)
+            if (c->dright >= 0) CKN(g_nccl.Send(slot + (long long)g.nx * plane, size_t(plane), ty, c->dright, c->comm, c->stream));
+            if (c->dleft >= 0) CKN(g_nccl.Recv(slot, size_t(plane), ty, c->dleft, c->comm, c->stream));
+        } else if (cv[3 * i] == -1) {
+            if (c->dleft >= 0) CKN(g_nccl.Send(slot - plane, size_t(plane), ty, c->dleft, c->comm, c->stream));
+            if (c->dright >= 0)
+                CKN(g_nccl.Recv(slot + (long long)(g.nx - 1) * plane, size_t(plane), ty, c->dright, c->comm, c->stream));
+        }
+    }
+    CKN(g_nccl.GroupEnd());
+    return record_progress(c);
 }
 
 template <typename T>
@@ -1681,7 +1721,8 @@ lbm_status dqq_step(lbm_ctx* c, long n) {
     // (measured faster than the one-step kernel for every lattice and dtype,
     // DESIGN.md section 11); an odd remainder (or, under AUTO, a driver
     // without the TMA encoder) one step at a time
-    for (bool k2 = c->opts.kernel != LBM_KERNEL_K1; k2 && n >= 2; n -= 2) {
+    const bool open = c->dg.xlo_open || c->dg.xhi_open;
+    for (bool k2 = c->opts.kernel != LBM_KERNEL_K1 && !open; k2 && n >= 2; n -= 2) {
         size_t slot = 0;
         lbm_status st = prof_begin(c, slot);
         if (st != LBM_OK) return st;
@@ -1707,6 +1748,7 @@ lbm_status dqq_step(lbm_ctx* c, long n) {
         c->launches++;
         c->k1_launches++;
         if ((st = prof_end(c, slot, (long long)c->dg.nx * c->dg.ny * c->dg.nz)) != LBM_OK) return st;
+        if (open && (st = dqq_exchange(c, static_cast<T*>(c->dbuf[c->dcur ^ 1]))) != LBM_OK) return st;
         c->dcur ^= 1;
         c->t += 1;
     }
@@ -1724,7 +1766,7 @@ lbm_status dqq_macro(lbm_ctx* c, double* rho, double* u, bool host) {
     }
     CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
     const long long plane = (long long)g.ny * g.nz;
-    const size_t stage_bytes = size_t(g.q) * size_t(g.pq) * c->esize;
+    const size_t stage_bytes = (size_t(g.q) * size_t(g.pq) - size_t(c->dorg)) * c->esize;
     const int cap = int(std::max<long long>(1, (long long)(stage_bytes / (4 * sizeof(double))) / plane));
     double* stage = static_cast<double*>(c->dbuf[c->dcur ^ 1]);
     for (int xb = 0; xb < g.nx; xb += cap) {
@@ -1747,7 +1789,7 @@ template <typename T>
 lbm_status dqq_box(lbm_ctx* c, int bx, int by, int bz, int lx, int ly, int lz, double* out) {
     const DqqGeom& g = c->dg;
     const long long bplane = (long long)ly * lz, bcells = (long long)lx * bplane;
-    const size_t stage_bytes = size_t(g.q) * size_t(g.pq) * c->esize;
+    const size_t stage_bytes = (size_t(g.q) * size_t(g.pq) - size_t(c->dorg)) * c->esize;
     const int cap = int(std::max<long long>(1, (long long)(stage_bytes / (size_t(g.q) * bplane * sizeof(double)))));
     double* stage = static_cast<double*>(c->dbuf[c->dcur ^ 1]);
     for (int xb = bx; xb < bx + lx; xb += cap) {
@@ -1944,9 +1986,11 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     }
     const int q = o.lattice == 0 ? 19 : o.lattice;
     if (q != 15 && q != 19 && q != 27) return fail(c, LBM_EINVAL, "bad lattice %d (15, 19 or 27)", o.lattice);
-    if (q != 19 && (o.comm != LBM_COMM_NONE || o.halo != LBM_HALO_AUTO || by > 1 ||
+    if (q != 19 && (o.comm == LBM_COMM_LOCAL || o.local_slabs > 1 || o.halo == LBM_HALO_PEER || by > 1 || ry > 1 ||
                     (o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K1 && o.kernel != LBM_KERNEL_K2)))
-        return fail(c, LBM_EINVAL, "lattice D3Q%d: one slab (comm NONE), kernel AUTO, K1 or K2", q);
+        return fail(c, LBM_EINVAL, "lattice D3Q%d: one slab per process (comm NONE or NCCL x-slabs), kernel AUTO, K1 or K2", q);
+    if (q != 19 && o.comm == LBM_COMM_NCCL && o.kernel == LBM_KERNEL_K2)
+        return fail(c, LBM_EINVAL, "lattice D3Q%d over NCCL x-slabs runs the one-step kernel (kernel AUTO or K1)", q);
     if (o.halo == LBM_HALO_PEER && o.comm != LBM_COMM_NCCL)
         return fail(c, LBM_EINVAL, "halo PEER needs comm NCCL (world 1: the periodic self-wrap)");
     if (o.halo == LBM_HALO_PEER && o.kernel != LBM_KERNEL_AUTO && o.kernel != LBM_KERNEL_K2)
@@ -2041,19 +2085,32 @@ lbm_status lbm_create_ex(lbm_ctx** out, int nx, int ny, int nz, double tau, cons
     if (q != 19) {  // D3Q15 / D3Q27: two canonical buffers, nothing else
         c->q = q;
         c->dg.q = q;
-        c->dg.nx = nx;
+        c->dg.nx = nxl;
         c->dg.ny = ny;
         c->dg.nz = nz;
         c->dg.nzp = round_up(nz, int(32 / c->esize));
         c->dg.bc = o.bc;
-        c->dg.pq = (long long)nx * ny * c->dg.nzp;
+        // NCCL x-slabs: one ghost plane per side per
+        // direction takes the pushes that leave the slab through a face shared
+        // with a neighbour rank (periodic: every face, world 1 included -- the
+        // wrap then travels through NCCL to this rank itself)
+        const bool nccl = o.comm == LBM_COMM_NCCL;
+        const bool per = o.bc == LBM_BC_PERIODIC;
+        c->dleft = nccl ? (per ? (o.rank - 1 + o.world) % o.world : (o.rank > 0 ? o.rank - 1 : -1)) : -1;
+        c->dright = nccl ? (per ? (o.rank + 1) % o.world : (o.rank < o.world - 1 ? o.rank + 1 : -1)) : -1;
+        c->dg.xlo_open = c->dleft >= 0;
+        c->dg.xhi_open = c->dright >= 0;
+        const int gh = nccl ? 1 : 0;
+        c->dg.pq = (long long)(nxl + 2 * gh) * ny * c->dg.nzp;
+        c->dorg = gh * (long long)ny * c->dg.nzp;
         const size_t bytes = size_t(q) * size_t(c->dg.pq) * c->esize;
         for (int b = 0; b < 2; ++b) {
-            if (cudaMalloc(&c->dbuf[b], bytes) != cudaSuccess) {
+            if (cudaMalloc(&c->dbase[b], bytes) != cudaSuccess) {
                 cudaGetLastError();
                 return bail(fail(c, LBM_ENOMEM, "cudaMalloc(%zu bytes)", bytes));
             }
-            if (cudaMemset(c->dbuf[b], 0, bytes) != cudaSuccess) return bail(fail(c, LBM_ECUDA, "cudaMemset"));
+            if (cudaMemset(c->dbase[b], 0, bytes) != cudaSuccess) return bail(fail(c, LBM_ECUDA, "cudaMemset"));
+            c->dbuf[b] = static_cast<char*>(c->dbase[b]) + c->dorg * (long long)c->esize;
         }
         if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(c, LBM_ECUDA, "create sync"));
         *out = c;
@@ -2249,7 +2306,7 @@ void lbm_destroy(lbm_ctx* c) {
     for (Slab& s : c->slabs)
         for (void* b : s.buf)
             if (b) cudaFree(b);
-    for (void* b : c->dbuf)
+    for (void* b : c->dbase)
         if (b) cudaFree(b);
     if (c->d_flag) cudaFree(c->d_flag);
     if (c->sc_sync) cudaFree(c->sc_sync);

@@ -231,11 +231,12 @@ __global__ void __launch_bounds__(256) k_dqq_step(const T* __restrict__ A, T* __
         int dx = x + cx, dy = y + cy, dz = z + cz;
         bool out = false;
         if constexpr (BC == BC_PERIODIC) {
-            dx = dx < 0 ? dx + g.nx : (dx >= g.nx ? dx - g.nx : dx);
+            if (!g.xlo_open) dx = dx < 0 ? dx + g.nx : (dx >= g.nx ? dx - g.nx : dx);  // else: ghost plane
             dy = dy < 0 ? dy + g.ny : (dy >= g.ny ? dy - g.ny : dy);
             dz = dz < 0 ? dz + g.nz : (dz >= g.nz ? dz - g.nz : dz);
         } else {
-            out = dx < 0 || dx >= g.nx || dy < 0 || dy >= g.ny || dz < 0 || dz >= g.nz;
+            out = (dx < 0 && !g.xlo_open) || (dx >= g.nx && !g.xhi_open) || dy < 0 || dy >= g.ny || dz < 0 ||
+                  dz >= g.nz;
         }
         if (!out) {
             __stcs(B + (long long)i * g.pq + ((long long)dx * g.ny + dy) * g.nzp + dz, f[i]);

@@ -61,6 +61,11 @@ cudaError_t launch_k3(const T* A, T* B, const StepParams<T>& P, cudaStream_t s);
 // collide + push step per launch; a single slab, no ghost planes.
 struct DqqGeom {
     int q, nx, ny, nz, nzp, bc;
+    // X-slab faces open to a neighbour slab (NCCL ranks): links leaving the
+    // slab through them are stored into the ghost plane x = -1 / nx (the
+    // buffers carry one per side) and moved by the halo exchange; a closed
+    // face is a wall (cavity) or wraps in the kernel (periodic, one slab)
+    int xlo_open, xhi_open;
     long long pq;  // elements per direction = nx * ny * nzp
 };
 template <typename T>

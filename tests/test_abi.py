@@ -137,6 +137,19 @@ def test_lattice_validation():
         lbm.lbm_create_ex(8, 8, 8, 0.6, None, "f64", o)
     with pytest.raises(lbm.LbmError):
         lbm.lbm_lattice_table(21)
+    # NCCL x-slabs of the other lattices: one-step kernel, x slabs only,
+    # NCCL send/recv (rejected before any allocation or communicator)
+    for kw, msg in [({"kernel": lbm.LBM_KERNEL_K2}, "one-step kernel"),
+                    ({"halo": lbm.LBM_HALO_PEER}, "D3Q15"),
+                    ({"ranks_y": 2}, "D3Q15")]:
+        o = lbm.lbm_default_opts()
+        o.lattice, o.comm, o.world, o.rank = 15, lbm.LBM_COMM_NCCL, 2, 0
+        uid = ctypes.create_string_buffer(128)  # (never used: validation fails first)
+        o.nccl_id = ctypes.cast(uid, ctypes.c_void_p)
+        for k, v in kw.items():
+            setattr(o, k, v)
+        with pytest.raises(lbm.LbmError, match=msg):
+            lbm.lbm_create_ex(8, 8, 8, 0.6, None, "f64", o)
 
 
 def test_xy_blocks_validation():

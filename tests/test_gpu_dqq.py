@@ -151,3 +151,38 @@ def test_two_step_sweep_degenerate_extents(q, dims, bc):
     assert np.array_equal(outs[0], outs[1])
     ref = oracle.dqq_run(q, f0, bc, 0.6, LID, 4)
     assert relerr_floor(outs[1], ref) <= TOL["f64"]
+
+
+@pytest.mark.parametrize("q", [15, 27])
+@pytest.mark.parametrize("bc", [lbm.LBM_BC_PERIODIC, lbm.LBM_BC_CAVITY])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_nccl_xslab_world1_bitwise(q, bc, dtype):
+    """D3Q15/27 over NCCL x-slabs (csrc/api.cu dqq_exchange; PAPER.md:336,
+    589-590) on hardware: a one-rank periodic communicator pushes the links
+    that leave the slab in x into its ghost planes and sends them to itself
+    (ncclSend/ncclRecv to self in one group) instead of wrapping in the
+    kernel; a one-rank cavity has walls on both faces.  One-step kernel,
+    odd and even step counts, set_populations / init / read-backs: bitwise
+    equal to the single-process context (whose K2Q two-step sweep equals the
+    one-step kernel bit for bit), and to the oracle."""
+    dims = (9, 6, 40)
+    f0 = li.uniform(90 + q, q * int(np.prod(dims)), 0.01, 0.06).reshape(q, *dims)
+    rho0 = li.uniform(91 + q, int(np.prod(dims)), 0.99, 1.01).reshape(dims)
+    try:
+        lbm.lbm_nccl_unique_id()
+    except lbm.LbmError as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    outs = []
+    for kw in ({}, {"comm": lbm.LBM_COMM_NCCL, "nccl_id": lbm.lbm_nccl_unique_id()}):
+        with lbm.Lattice(*dims, 0.6, LID, dtype, bc=bc, lattice=q, **kw) as lat:
+            lat.set_populations(f0)
+            lat.step(3)
+            lat.step(2)
+            a = lat.populations()
+            rho, u = lat.macroscopic()
+            lat.init_equilibrium(rho0, None)
+            lat.step(4)
+            outs.append((a, rho, u, lat.populations(), lat.populations_box(2, 1, 3, 5, 4, 30)))
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
+    assert relerr_floor(outs[1][0], oracle.dqq_run(q, f0, bc, 0.6, LID, 5)) <= TOL[dtype]
