@@ -1688,8 +1688,10 @@ lbm_status dqq_set(lbm_ctx* c, const double* f) {
 // X-slab halo of a D3Q15/27 NCCL slab after a push step (B = f(t+1)): the
 // populations pushed into ghost plane x = nx (c_x = +1) belong to plane 0
 // of the right neighbour, those in ghost plane x = -1 (c_x = -1) to plane
-// nx - 1 of the left one -- per direction one contiguous (y, z) plane,
-// which no rank writes otherwise (its source lies across the face)
+// nx - 1 of the left one -- per direction one contiguous (y, z) plane.  They
+// arrive in the receiver's unused ghost slots of the same direction and a
+// merge kernel copies them in, skipping the cells whose link source lies
+// beyond a y / z wall (their slot holds the cell's own bounce-back)
 template <typename T>
 lbm_status dqq_exchange(lbm_ctx* c, T* B) {
     const DqqGeom& g = c->dg;
@@ -1698,19 +1700,22 @@ lbm_status dqq_exchange(lbm_ctx* c, T* B) {
     int cv[27 * 3];
     double wv[27];
     dqq_table(g.q, cv, wv);
+    T* const lo = B - plane;                    // ghost plane x = -1 of slot 0
+    T* const hi = B + (long long)g.nx * plane;  // ghost plane x = nx of slot 0
     CKN(g_nccl.GroupStart());
     for (int i = 0; i < g.q; ++i) {
-        T* const slot = B + (long long)i * g.pq;
+        const long long off = (long long)i * g.pq;
         if (cv[3 * i] == 1) {  // [send right, recv left]: pairs match when left == right (two ranks, or itself)
-            if (c->dright >= 0) CKN(g_nccl.Send(slot + (long long)g.nx * plane, size_t(plane), ty, c->dright, c->comm, c->stream));
-            if (c->dleft >= 0) CKN(g_nccl.Recv(slot, size_t(plane), ty, c->dleft, c->comm, c->stream));
+            if (c->dright >= 0) CKN(g_nccl.Send(hi + off, size_t(plane), ty, c->dright, c->comm, c->stream));
+            if (c->dleft >= 0) CKN(g_nccl.Recv(lo + off, size_t(plane), ty, c->dleft, c->comm, c->stream));
         } else if (cv[3 * i] == -1) {
-            if (c->dleft >= 0) CKN(g_nccl.Send(slot - plane, size_t(plane), ty, c->dleft, c->comm, c->stream));
-            if (c->dright >= 0)
-                CKN(g_nccl.Recv(slot + (long long)(g.nx - 1) * plane, size_t(plane), ty, c->dright, c->comm, c->stream));
+            if (c->dleft >= 0) CKN(g_nccl.Send(lo + off, size_t(plane), ty, c->dleft, c->comm, c->stream));
+            if (c->dright >= 0) CKN(g_nccl.Recv(hi + off, size_t(plane), ty, c->dright, c->comm, c->stream));
         }
     }
     CKN(g_nccl.GroupEnd());
+    CK(launch_dqq_merge<T>(B, g, c->stream));
+    c->launches++;
     return record_progress(c);
 }
 

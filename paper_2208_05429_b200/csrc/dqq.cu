@@ -252,6 +252,35 @@ __global__ void __launch_bounds__(256) k_dqq_step(const T* __restrict__ A, T* __
     });
 }
 
+// X-slab halo merge (NCCL slabs, api.cu dqq_exchange): the populations a
+// neighbour rank pushed across an open face arrive in this rank's unused
+// ghost slots (c_x = +1 directions in ghost plane -1, c_x = -1 ones in
+// ghost plane nx) and are copied into plane 0 / nx - 1 -- except where the
+// link's source lies beyond a y / z wall (cavity), whose slot the cell's own
+// bounce-back (lid included) already wrote this step
+template <typename T, int Q, int BC>
+__global__ void __launch_bounds__(256) k_dqq_merge(T* __restrict__ B, DqqGeom g) {
+    const int z = blockIdx.x * 32 + threadIdx.x;
+    const int y = blockIdx.y * 8 + threadIdx.y;
+    const int side = blockIdx.z;  // 0: face x = 0 (from the left rank), 1: face x = nx - 1
+    if (z >= g.nz || y >= g.ny || !(side ? g.xhi_open : g.xlo_open)) return;
+    const long long plane = (long long)g.ny * g.nzp, yz = (long long)y * g.nzp + z;
+    static_for<0, Q>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        constexpr int cx = dqq_c<Q>(i, 0), cy = dqq_c<Q>(i, 1), cz = dqq_c<Q>(i, 2);
+        if constexpr (cx != 0) {
+            if ((cx > 0) == (side == 0)) {
+                const bool inside = BC == BC_PERIODIC || ((unsigned)(y - cy) < (unsigned)g.ny &&
+                                                          (unsigned)(z - cz) < (unsigned)g.nz);
+                const long long own = side ? (long long)(g.nx - 1) * plane : 0;
+                const long long ghost = side ? (long long)g.nx * plane : -plane;
+                T* const slot = B + (long long)i * g.pq;
+                if (inside) slot[own + yz] = slot[ghost + yz];
+            }
+        }
+    });
+}
+
 // canonical feq(rho, u) (rho / u NULL: 1 / 0)
 template <typename T, int Q>
 __global__ void __launch_bounds__(256) k_dqq_init(const double* __restrict__ rho, const double* __restrict__ u,
@@ -636,7 +665,24 @@ __global__ void __launch_bounds__(KQCfg<T, Q, TY, TZ, WS>::NT, KQCfg<T, Q, TY, T
 namespace {
 dim3 dqq_grid(int nz, int ny, int nx) { return dim3((nz + 31) / 32, (ny + 7) / 8, nx); }
 const dim3 kDqqBlock(32, 8, 1);
+
+
 }  // namespace
+
+template <typename T>
+cudaError_t launch_dqq_merge(T* B, const DqqGeom& g, cudaStream_t s) {
+    const dim3 grid = dqq_grid(g.nz, g.ny, 2);
+#define MERGE(Q)                                                                               \
+    if (g.bc == BC_PERIODIC) k_dqq_merge<T, Q, BC_PERIODIC><<<grid, kDqqBlock, 0, s>>>(B, g); \
+    else k_dqq_merge<T, Q, BC_CAVITY><<<grid, kDqqBlock, 0, s>>>(B, g);
+    switch (g.q) {
+        case 15: MERGE(15) break;
+        case 27: MERGE(27) break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef MERGE
+    return cudaGetLastError();
+}
 
 #define LBM_DQQ_DISPATCH(call)                      \
     switch (g.q) {                                  \
@@ -805,7 +851,8 @@ void dqq_table(int q, int* c, double* w) {
     template cudaError_t launch_dqq_box<T>(const T*, const DqqGeom&, int, int, int, int, int, int, double*,    \
                                            cudaStream_t);                                                      \
     template cudaError_t launch_dqq_import<T>(const double*, T*, const DqqGeom&, int, int, cudaStream_t);     \
-    template cudaError_t launch_dqq_k2<T>(const T*, T*, const DqqGeom&, T, const double*, cudaStream_t);
+    template cudaError_t launch_dqq_k2<T>(const T*, T*, const DqqGeom&, T, const double*, cudaStream_t);     \
+    template cudaError_t launch_dqq_merge<T>(T*, const DqqGeom&, cudaStream_t);
 LBM_DQQ_INST(double)
 LBM_DQQ_INST(float)
 #undef LBM_DQQ_INST

@@ -86,6 +86,8 @@ void dqq_table(int q, int* c, double* w);
 // driver has no TMA descriptor encoder.
 template <typename T>
 cudaError_t launch_dqq_k2(const T* A, T* B, const DqqGeom& g, T omega, const double ulid[3], cudaStream_t s);
+template <typename T>
+cudaError_t launch_dqq_merge(T* B, const DqqGeom& g, cudaStream_t s);
 
 // k2.cu helpers shared with dqq.cu: cuTensorMapEncodeTiled (null if the
 // driver lacks it), the current device's SM count and ordinal
